@@ -1,0 +1,214 @@
+/*
+ * velan_gpu.h — C-ABI of the B200-native semblance parameter search.
+ *
+ * This is the drop-in boundary for the hot path of the reference library
+ * "velan" (/root/reference/proj/include/velan, header-only C++20).  The
+ * reference has no FFI; its replacement seam is the pipeline layer:
+ *
+ *   velan::run_cmp(const Dataset&, const ScanConfig&, int workers,
+ *                  CacheStats*)                       cmp_pipeline.hpp:94-106
+ *   velan::run_crs(const Dataset&, const ScanConfig&, GridDims, double apm,
+ *                  const CrsOptions&, CrsRunInfo*, CacheStats*)
+ *                                                     crs_pipeline.hpp:283-460
+ *   velan::scan_cdp(gather, cfg)                       cmp_pipeline.hpp:17-27
+ *   velan::scan_central_cdp(central, neighbors, cfg)   crs_pipeline.hpp:184-197
+ *
+ * Every entry point below replaces one of those (cited per function).  The
+ * signatures are plain C: host pointers and sizes, no torch or velan types,
+ * no exceptions.  Errors are status codes that map 1:1 onto the reference's
+ * exception hierarchy (error.hpp:9-40); the message of the last failure on
+ * the calling thread is available from velan_gpu_last_error().
+ *
+ * Data layout (mirrors velan::Dataset, types.hpp:14-54, flattened):
+ *   samples  fp32 [n_gathers][max_traces][ns]  (trace-contiguous, as
+ *                                               Trace::samples)
+ *   coords   fp32 [n_gathers][max_traces][4]   (sx, sy, gx, gy)
+ *   ntraces  i32  [n_gathers]                  (traces actually present)
+ *   cdp_id   u32  [n_gathers]
+ * Half-offsets (compute_halfpoints, traveltime.hpp:16-27) and midpoints
+ * (midpoint_of, types.hpp:57-62) are derived from coords on the host with the
+ * reference's fp32 expressions, so results are bit-comparable.
+ */
+#ifndef VELAN_GPU_H_
+#define VELAN_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VELAN_GPU_ABI_VERSION 1
+
+/* Status codes.  0 = success.  Config and parameter errors are raised before
+ * any device work, like ScanConfig::validate (scan.hpp:61-78). */
+enum {
+  VELAN_GPU_OK = 0,
+  VELAN_GPU_ECONFIG = 1,  /* velan::config_error    (error.hpp:19-22) */
+  VELAN_GPU_EPARAM = 2,   /* velan::parameter_error (error.hpp:14-17) */
+  VELAN_GPU_ERUNTIME = 3, /* velan::error: worker/device failure       */
+  VELAN_GPU_ENODEV = 4    /* no usable sm_100 device                    */
+};
+
+/* Moveout operator evaluated per (pair, trace).
+ *  NMO     t = sqrt(t0^2 + 4 h2 / v^2)                traveltime.hpp:59-61
+ *  CRS_D2  t = sqrt(t0^2 + (4 h2 + d2) / v^2)         traveltime.hpp:53-56
+ *          (the reference's neighbourhood operator, d2 = |dm|^2)
+ *  CRS_ABC t = sqrt((t0 + 2 A dm)^2 + 2 t0 B dm^2 + 4 h2 / v^2)
+ *          (BASELINE.json's three-parameter operator; C = 2/(t0 v^2) is
+ *          scanned through v.  No reference implementation exists, see
+ *          DESIGN.md §3 for the exact fp32 evaluation order.) */
+typedef enum {
+  VELAN_OP_NMO = 0,
+  VELAN_OP_CRS_D2 = 1,
+  VELAN_OP_CRS_ABC = 2
+} velan_operator;
+
+/* Kernel variant, the GPU analogue of velan::KernelVariant (scan.hpp:14-23).
+ *  EXACT  every fp32 operation in the reference order and rounding: the
+ *         semblance matrix, picks and stack are bitwise identical to
+ *         velan::scan_tile_blocked + scan_sweep (kernel.hpp:276-316,
+ *         scan.hpp:108-181).
+ *  FAST   restructured accumulation (the production variant): picks and hit
+ *         indices identical, semblance/stack within 1e-4 relative. */
+typedef enum { VELAN_VARIANT_EXACT = 0, VELAN_VARIANT_FAST = 1 } velan_variant;
+
+typedef enum { VELAN_MEM_HOST = 0, VELAN_MEM_DEVICE = 1 } velan_mem;
+
+typedef struct velan_gpu_dataset {
+  int32_t n_gathers;
+  int32_t max_traces; /* stride of the trace axis (Dataset::fold)          */
+  int32_t ns;         /* CdpGather::ns, shared by every gather            */
+  uint32_t dt_us;     /* CdpGather::dt_us                                  */
+  const uint32_t* cdp_id;  /* host [n_gathers]                             */
+  const int32_t* ntraces;  /* host [n_gathers]                             */
+  const float* coords;     /* host [n_gathers][max_traces][4]              */
+  const float* samples;    /* [n_gathers][max_traces][ns], see samples_mem */
+  int32_t samples_mem;     /* velan_mem                                    */
+  int32_t samples_device;  /* CUDA ordinal when samples_mem == DEVICE      */
+} velan_gpu_dataset;
+
+typedef struct velan_gpu_scan {
+  int32_t op;      /* velan_operator                                      */
+  int32_t variant; /* velan_variant                                       */
+  int32_t w;       /* ScanConfig::w, window length in samples (1..32)     */
+  /* Candidate axes.  Flat candidate index = (ia * n_b + ib) * n_c + ic;
+   * NMO / CRS_D2 use n_a = n_b = 1.  Lowest flat index wins exact ties,
+   * like scan_sweep's strict '>' (scan.hpp:167-179). */
+  int32_t n_a, n_b, n_c;
+  const float* a; /* host [n_a]  A, s/m          (CRS_ABC only)           */
+  const float* b; /* host [n_b]  B, s/m^2        (CRS_ABC only)           */
+  const float* v; /* host [n_c]  velocity, m/s   (all operators)          */
+  double apm;     /* CRS: closed-ball radius in m (neighbors_of,
+                     crs_pipeline.hpp:162-180); ignored for NMO           */
+} velan_gpu_scan;
+
+typedef struct velan_gpu_result {
+  /* Caller-allocated outputs, row r = output midpoint r.  CMP rows follow
+   * input order (run_cmp); CRS rows follow cdp_id order, ties by input index
+   * (run_crs, crs_pipeline.hpp:449-459). */
+  int32_t out_mem;        /* velan_mem of the four arrays               */
+  int32_t* best_idx;      /* [n_gathers][ns] flat candidate index       */
+  float* best_semblance;  /* [n_gathers][ns]  BestPick::semblance       */
+  float* best_stack;      /* [n_gathers][ns]  SemblanceMatrix::stack_trace */
+  float* matrix;          /* optional [n_gathers][ns][n_cand] (values),
+                             NULL = not emitted                         */
+  int32_t* row_gather;    /* optional [n_gathers]: input index per row  */
+  /* Filled by the call. */
+  uint64_t valid_intersections;   /* CacheStats::naive_fetches          */
+  uint64_t nominal_intersections; /* rows * ns * n_cand * traces/sweep  */
+  double kernel_ms;  /* device time of the scan kernels, max over devices */
+  double total_ms;   /* wall time of the whole call                       */
+} velan_gpu_result;
+
+typedef struct velan_gpu_ctx velan_gpu_ctx;
+typedef struct velan_gpu_plan velan_gpu_plan;
+
+/* ABI version and the message of the last failure on this thread. */
+int velan_gpu_abi_version(void);
+const char* velan_gpu_last_error(void);
+/* Number of visible sm_100 devices (0 on a host without GPU). */
+int velan_gpu_device_count(void);
+
+/* Context: owns per-device streams, events and cached device buffers.
+ * device_ids may be NULL (then devices 0..n_devices-1).  Replaces the
+ * std::thread worker pool of parallel_for_indexed (cmp_pipeline.hpp:34-88):
+ * midpoints are split into contiguous blocks, one host thread per device. */
+int velan_gpu_create(const int32_t* device_ids, int32_t n_devices,
+                     velan_gpu_ctx** out);
+void velan_gpu_destroy(velan_gpu_ctx* ctx);
+
+/* Validate a scan without touching a device; mirrors ScanConfig::validate
+ * (scan.hpp:61-78) and scan_sweep's ns > w + 1 check (scan.hpp:113-114). */
+int velan_gpu_validate(const velan_gpu_dataset* ds, const velan_gpu_scan* sc);
+
+/* One-shot scans over host buffers (host->device, kernels, device->host).
+ *  velan_gpu_cmp  replaces run_cmp   (cmp_pipeline.hpp:94-106); op NMO.
+ *  velan_gpu_crs  replaces run_crs   (crs_pipeline.hpp:283-460) on a 1-D
+ *                 contiguous shard layout; op CRS_D2 or CRS_ABC.
+ * Both are synchronous, deterministic and bitwise independent of the number
+ * of devices (the reference's worker-count invariance,
+ * test_cmp_pipeline.cpp:122-140). */
+int velan_gpu_cmp(velan_gpu_ctx* ctx, const velan_gpu_dataset* ds,
+                  const velan_gpu_scan* sc, velan_gpu_result* res);
+int velan_gpu_crs(velan_gpu_ctx* ctx, const velan_gpu_dataset* ds,
+                  const velan_gpu_scan* sc, velan_gpu_result* res);
+
+/* Resident plans (single device): tables and samples stay in HBM across
+ * executions.  samples may already be device memory (samples_mem DEVICE).
+ * execute runs on `stream` (a cudaStream_t, NULL = the plan's own stream)
+ * and leaves outputs where res->out_mem says. */
+int velan_gpu_plan_create(velan_gpu_ctx* ctx, const velan_gpu_dataset* ds,
+                          const velan_gpu_scan* sc, velan_gpu_plan** out);
+int velan_gpu_plan_execute(velan_gpu_plan* plan, velan_gpu_result* res,
+                           void* stream);
+/* Kernel launches one execute issues (for launch accounting). */
+int velan_gpu_plan_launches(const velan_gpu_plan* plan);
+void velan_gpu_plan_destroy(velan_gpu_plan* plan);
+
+/* hit_for (traveltime.hpp:66-80) evaluated by the device code path of the
+ * given variant, for n traveltimes t (host arrays).  Test hook for the
+ * index arithmetic: k1 and valid must match the reference bit for bit. */
+int velan_gpu_hit_batch(const float* t, int32_t n, double dt_s, int32_t ns,
+                        int32_t w, int32_t variant, int32_t* k1, float* x,
+                        uint8_t* valid);
+
+/* Seeded synthetic inputs of the BASELINE.json configs, generated on the
+ * host with per-gather counter-based streams (order-free, reproducible for
+ * any thread count).  kind: 0 = CMP (hyperbolic events), 1 = CRS line
+ * (dipping curved reflectors).  Fills caller buffers shaped like
+ * velan_gpu_dataset (samples [G][M][ns], coords [G][M][4], ntraces,
+ * cdp_id).  See DESIGN.md §6 for the event model. */
+typedef struct velan_gpu_synth {
+  int32_t kind;
+  int32_t n_gathers, n_traces, ns;
+  uint32_t dt_us;
+  double spacing;           /* midpoint spacing, m                     */
+  double h0, dh;            /* half-offset of trace m = h0 + m * dh    */
+  int32_t n_events;
+  double t0_lo, t0_hi;      /* event zero-offset time range, s         */
+  double v_lo, v_hi;        /* event velocity range (CMP-small, CRS)   */
+  int32_t v_profile;        /* CMP: 0 = uniform v, 1 = v(t0) trend     */
+  double v_trend_0, v_trend_slope, v_perturb; /* v = (v0 + s t0)(1+eps) */
+  double amp_lo, amp_hi;
+  double freq;              /* Ricker peak frequency, Hz               */
+  double sigma;             /* Gaussian noise sigma                    */
+  double a_abs, b_max;      /* CRS: A ~ U[-a_abs, a_abs], B ~ U[0,b_max] */
+  uint64_t seed;
+  int32_t gather_first;     /* generate gathers [first, first+n) of the
+                               full line (for sharded generation)      */
+  int32_t n_line;           /* gathers in the full line (0 = n_gathers);
+                               CRS reflector positions span it         */
+  int32_t n_threads;        /* 0 = hardware concurrency                */
+} velan_gpu_synth;
+
+int velan_gpu_synth_generate(const velan_gpu_synth* p, float* samples,
+                             float* coords, int32_t* ntraces,
+                             uint32_t* cdp_id);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* VELAN_GPU_H_ */

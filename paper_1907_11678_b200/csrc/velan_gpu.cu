@@ -1,0 +1,1014 @@
+// velan_gpu.cu — host runtime of the C-ABI (include/velan_gpu.h).
+//
+// Replaces the reference's pipeline layer (cmp_pipeline.hpp, crs_pipeline.hpp)
+// for the hot path:
+//   * validation before any device work (ScanConfig::validate, scan.hpp:61-78;
+//     scan_sweep's ns > w + 1, scan.hpp:113-114; partition's apm > 0,
+//     crs_pipeline.hpp:95-98);
+//   * TraceSweep construction on the host: h2 per trace (traveltime.hpp:16-27),
+//     midpoints (types.hpp:57-62), the CRS neighbourhood as a closed ball in
+//     cdp_id order (crs_pipeline.hpp:162-180) with fp32 d2 (kernel.hpp:86-91);
+//   * data parallelism: contiguous blocks of output rows per device, each
+//     device receiving its rows' gathers plus the CRS halo (replicated, no
+//     collective), one host thread per device — the B200 form of
+//     parallel_for_indexed (cmp_pipeline.hpp:34-88) and of run_crs's shards;
+//   * H2D staging overlapped with compute: rows are launched in waves, the
+//     copy stream uploads the gathers a wave needs while the previous wave
+//     computes;
+//   * results in input order (CMP) or cdp_id order (CRS, crs_pipeline.hpp:
+//     449-459), bitwise independent of the device count.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/velan_gpu.h"
+#include "semblance_kernels.cuh"
+
+namespace velan_gpu {
+namespace {
+
+thread_local std::string g_last_error;
+
+struct ApiError : std::runtime_error {
+  int code;
+  ApiError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file,
+                             int line) {
+  char buf[512];
+  std::snprintf(buf, sizeof buf, "CUDA error %s (%s) in %s at %s:%d",
+                cudaGetErrorName(e), cudaGetErrorString(e), what, file, line);
+  throw ApiError(VELAN_GPU_ERUNTIME, buf);
+}
+#define VG_CUDA(expr)                                              \
+  do {                                                             \
+    cudaError_t e_ = (expr);                                       \
+    if (e_ != cudaSuccess) throw_cuda(e_, #expr, __FILE__, __LINE__); \
+  } while (0)
+
+constexpr int kMaxW = 32;
+
+// ---------------------------------------------------------------------------
+// Kernel dispatch: (operator kind, variant, window) -> instantiation.
+
+using KernelFn = void (*)(ScanParams);
+
+struct KernelChoice {
+  KernelFn fn = nullptr;
+  int cc = 0;
+};
+
+template <int OPK, int VAR, int WMAX, bool FIXED>
+KernelChoice pick() {
+  constexpr int CC = WMAX > 16 ? 2 : 4;
+  return KernelChoice{&semblance_scan_kernel<OPK, VAR, WMAX, FIXED, CC>, CC};
+}
+
+template <int OPK, int VAR>
+KernelChoice pick_w(int w) {
+  switch (w) {
+    case 1: return pick<OPK, VAR, 1, true>();
+    case 2: return pick<OPK, VAR, 2, true>();
+    case 4: return pick<OPK, VAR, 4, true>();
+    case 8: return pick<OPK, VAR, 8, true>();
+    case 11: return pick<OPK, VAR, 11, true>();
+    case 15: return pick<OPK, VAR, 15, true>();
+    case 16: return pick<OPK, VAR, 16, true>();
+    default: break;
+  }
+  if (w <= 4) return pick<OPK, VAR, 4, false>();
+  if (w <= 8) return pick<OPK, VAR, 8, false>();
+  if (w <= 16) return pick<OPK, VAR, 16, false>();
+  return pick<OPK, VAR, 32, false>();
+}
+
+KernelChoice choose_kernel(int op, int variant, int w) {
+  const int opk = op == VELAN_OP_CRS_ABC ? OPK_ABC : OPK_Q;
+  if (opk == OPK_Q)
+    return variant == VELAN_VARIANT_EXACT ? pick_w<OPK_Q, VAR_EXACT>(w)
+                                          : pick_w<OPK_Q, VAR_FAST>(w);
+  return variant == VELAN_VARIANT_EXACT ? pick_w<OPK_ABC, VAR_EXACT>(w)
+                                        : pick_w<OPK_ABC, VAR_FAST>(w);
+}
+
+// ---------------------------------------------------------------------------
+// Validation (before any device work).
+
+std::string fmt(const char* f, long long a = 0, long long b = 0) {
+  char buf[256];
+  std::snprintf(buf, sizeof buf, f, a, b);
+  return buf;
+}
+
+void validate(const velan_gpu_dataset* ds, const velan_gpu_scan* sc,
+              bool crs) {
+  if (!ds || !sc) throw ApiError(VELAN_GPU_EPARAM, "null dataset or scan");
+  // ScanConfig::validate (scan.hpp:61-78)
+  if (sc->w < 1) throw ApiError(VELAN_GPU_ECONFIG, "ScanConfig: w must be >= 1");
+  if (sc->n_c < 1)
+    throw ApiError(VELAN_GPU_ECONFIG, "ScanConfig: nc must be >= 1");
+  if (sc->op != VELAN_OP_NMO && sc->op != VELAN_OP_CRS_D2 &&
+      sc->op != VELAN_OP_CRS_ABC)
+    throw ApiError(VELAN_GPU_ECONFIG, "ScanConfig: unknown moveout operator");
+  if (sc->variant != VELAN_VARIANT_EXACT && sc->variant != VELAN_VARIANT_FAST)
+    throw ApiError(VELAN_GPU_ECONFIG, "ScanConfig: unknown kernel variant");
+  if (crs && sc->op == VELAN_OP_NMO)
+    throw ApiError(VELAN_GPU_ECONFIG,
+                   "velan_gpu_crs: operator must be CRS_D2 or CRS_ABC");
+  if (!crs && sc->op != VELAN_OP_NMO)
+    throw ApiError(VELAN_GPU_ECONFIG, "velan_gpu_cmp: operator must be NMO");
+  if (sc->w > kMaxW)
+    throw ApiError(VELAN_GPU_ECONFIG,
+                   fmt("ScanConfig: w = %lld exceeds the GPU kernels' maximum "
+                       "window of %lld samples",
+                       sc->w, kMaxW));
+  if (!sc->v) throw ApiError(VELAN_GPU_EPARAM, "velocity candidates are null");
+  for (int c = 0; c < sc->n_c; ++c)
+    if (!(sc->v[c] > 0.0f) || !std::isfinite(sc->v[c]))
+      throw ApiError(VELAN_GPU_ECONFIG,
+                     "ScanConfig: need 0 < v for every velocity candidate");
+  if (sc->op == VELAN_OP_CRS_ABC) {
+    if (sc->n_a < 1 || sc->n_b < 1 || !sc->a || !sc->b)
+      throw ApiError(VELAN_GPU_ECONFIG,
+                     "ScanConfig: CRS_ABC needs n_a >= 1 and n_b >= 1");
+    for (int i = 0; i < sc->n_a; ++i)
+      if (!std::isfinite(sc->a[i]))
+        throw ApiError(VELAN_GPU_ECONFIG, "ScanConfig: non-finite A candidate");
+    for (int i = 0; i < sc->n_b; ++i)
+      if (!std::isfinite(sc->b[i]))
+        throw ApiError(VELAN_GPU_ECONFIG, "ScanConfig: non-finite B candidate");
+    const long long nc = 1LL * sc->n_a * sc->n_b * sc->n_c;
+    if (nc > (1LL << 30))
+      throw ApiError(VELAN_GPU_ECONFIG, "ScanConfig: too many candidates");
+  }
+  // dataset shape
+  if (ds->n_gathers < 0) throw ApiError(VELAN_GPU_EPARAM, "n_gathers < 0");
+  if (ds->n_gathers == 0) return;  // run_cmp / run_crs return {} (no error)
+  if (crs && !(sc->apm > 0.0))
+    throw ApiError(VELAN_GPU_ECONFIG, "partition: apm must be > 0");
+  if (ds->max_traces < 1)
+    throw ApiError(VELAN_GPU_EPARAM, "max_traces must be >= 1");
+  if (ds->dt_us == 0) throw ApiError(VELAN_GPU_EPARAM, "dt must be > 0");
+  if (!ds->ntraces || !ds->coords || !ds->samples || !ds->cdp_id)
+    throw ApiError(VELAN_GPU_EPARAM, "dataset arrays are null");
+  if (ds->samples_mem != VELAN_MEM_HOST && ds->samples_mem != VELAN_MEM_DEVICE)
+    throw ApiError(VELAN_GPU_EPARAM, "samples_mem must be HOST or DEVICE");
+  // scan_sweep: the window plus its interpolation neighbour must fit
+  if (ds->ns <= sc->w + 1)
+    throw ApiError(VELAN_GPU_ECONFIG,
+                   "scan_sweep: window does not fit trace length");
+  if (ds->ns > 24000)
+    throw ApiError(VELAN_GPU_ECONFIG,
+                   "ns > 24000 exceeds the shared-memory staging capacity");
+  for (int g = 0; g < ds->n_gathers; ++g) {
+    if (ds->ntraces[g] < 0 || ds->ntraces[g] > ds->max_traces)
+      throw ApiError(VELAN_GPU_EPARAM,
+                     fmt("gather %lld: ntraces outside [0, max_traces]", g));
+  }
+  for (int g = 0; g < ds->n_gathers; ++g)
+    if (ds->ntraces[g] == 0) {
+      if (crs)  // partition -> midpoint_of throws (crs_pipeline.hpp:104)
+        throw ApiError(VELAN_GPU_EPARAM, "midpoint_of: gather has no traces");
+      // run_cmp: the worker's TraceSweep throws, the pool wraps it
+      // (cmp_pipeline.hpp:77-85, kernel.hpp:100-101)
+      throw ApiError(
+          VELAN_GPU_ERUNTIME,
+          fmt("worker pool failure after 0 of %lld jobs: TraceSweep: central "
+              "gather has no traces (gather %lld)",
+              ds->n_gathers, g));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Host-side sweep construction.
+
+struct HostSweep {
+  int G = 0, M = 0, ns = 0, rows = 0;
+  int op = 0, w = 0, n_a = 1, n_b = 1, n_c = 1, ncand = 1;
+  double dt = 0.0;
+  std::vector<float> h2;          // [G][M]
+  std::vector<float> mx, my;      // [G]
+  std::vector<int> row_gather;    // [rows]
+  std::vector<int> leg_off;       // [rows + 1]
+  std::vector<int> leg_gather;    // global gather index
+  std::vector<float> leg_d2, leg_dm;
+  std::vector<long long> row_traces;  // traces per sweep
+  std::vector<float> t0;          // [ns]
+  std::vector<float> a, b, v;
+};
+
+HostSweep build_sweep(const velan_gpu_dataset* ds, const velan_gpu_scan* sc) {
+  HostSweep h;
+  h.G = ds->n_gathers;
+  h.M = ds->max_traces;
+  h.ns = ds->ns;
+  h.op = sc->op;
+  h.w = sc->w;
+  h.n_a = sc->op == VELAN_OP_CRS_ABC ? sc->n_a : 1;
+  h.n_b = sc->op == VELAN_OP_CRS_ABC ? sc->n_b : 1;
+  h.n_c = sc->n_c;
+  h.ncand = h.n_a * h.n_b * h.n_c;
+  h.dt = static_cast<double>(ds->dt_us) * 1e-6;  // CdpGather::dt_seconds
+  h.v.assign(sc->v, sc->v + sc->n_c);
+  if (sc->op == VELAN_OP_CRS_ABC) {
+    h.a.assign(sc->a, sc->a + sc->n_a);
+    h.b.assign(sc->b, sc->b + sc->n_b);
+  } else {
+    h.a.assign(1, 0.0f);
+    h.b.assign(1, 0.0f);
+  }
+  // t0_k = float(k * dt_s), scan.hpp:133
+  h.t0.resize(h.ns);
+  for (int k = 0; k < h.ns; ++k) h.t0[k] = static_cast<float>(k * h.dt);
+  // compute_halfpoints (traveltime.hpp:16-27) and midpoint_of
+  h.h2.assign(static_cast<size_t>(h.G) * h.M, 0.0f);
+  h.mx.assign(h.G, 0.0f);
+  h.my.assign(h.G, 0.0f);
+  for (int g = 0; g < h.G; ++g) {
+    for (int m = 0; m < ds->ntraces[g]; ++m) {
+      const float* c4 = ds->coords + (static_cast<size_t>(g) * h.M + m) * 4;
+      const float dx = c4[2] - c4[0];
+      const float dy = c4[3] - c4[1];
+      h.h2[static_cast<size_t>(g) * h.M + m] = (dx * dx + dy * dy) * 0.25f;
+    }
+    const float* c0 = ds->coords + static_cast<size_t>(g) * h.M * 4;
+    h.mx[g] = (c0[0] + c0[2]) * 0.5f;
+    h.my[g] = (c0[1] + c0[3]) * 0.5f;
+  }
+  // output rows
+  h.rows = h.G;
+  h.row_gather.resize(h.G);
+  std::iota(h.row_gather.begin(), h.row_gather.end(), 0);
+  if (sc->op != VELAN_OP_NMO)
+    std::stable_sort(h.row_gather.begin(), h.row_gather.end(),
+                     [&](int x, int y) { return ds->cdp_id[x] < ds->cdp_id[y]; });
+  h.leg_off.assign(1, 0);
+  h.row_traces.resize(h.rows);
+  if (sc->op == VELAN_OP_NMO) {
+    for (int r = 0; r < h.rows; ++r) {
+      const int g = h.row_gather[r];
+      h.leg_gather.push_back(g);
+      h.leg_d2.push_back(0.0f);
+      h.leg_dm.push_back(0.0f);
+      h.leg_off.push_back(static_cast<int>(h.leg_gather.size()));
+      h.row_traces[r] = ds->ntraces[g];
+    }
+    return h;
+  }
+  // CRS neighbourhoods: closed ball |dm| <= apm (double compare of the
+  // fp32 difference, crs_pipeline.hpp:172-174), self excluded, empty
+  // gathers skipped (kernel.hpp:87), cdp_id order (crs_pipeline.hpp:176-179)
+  std::vector<int> by_x(h.G);
+  std::iota(by_x.begin(), by_x.end(), 0);
+  std::sort(by_x.begin(), by_x.end(),
+            [&](int x, int y) { return h.mx[x] < h.mx[y]; });
+  std::vector<double> xs(h.G);
+  for (int i = 0; i < h.G; ++i) xs[i] = h.mx[by_x[i]];
+  const double apm = sc->apm;
+  const double margin = apm * 1e-5 + 1e-3;
+  std::vector<int> nb;
+  for (int r = 0; r < h.rows; ++r) {
+    const int g = h.row_gather[r];
+    nb.clear();
+    const auto lo = std::lower_bound(xs.begin(), xs.end(),
+                                     static_cast<double>(h.mx[g]) - apm - margin);
+    const auto hi = std::upper_bound(xs.begin(), xs.end(),
+                                     static_cast<double>(h.mx[g]) + apm + margin);
+    for (auto it = lo; it != hi; ++it) {
+      const int o = by_x[it - xs.begin()];
+      if (o == g || ds->ntraces[o] == 0) continue;
+      const double dx = static_cast<double>(h.mx[o] - h.mx[g]);
+      const double dy = static_cast<double>(h.my[o] - h.my[g]);
+      if (dx * dx + dy * dy <= apm * apm) nb.push_back(o);
+    }
+    std::sort(nb.begin(), nb.end(), [&](int x, int y) {
+      return ds->cdp_id[x] != ds->cdp_id[y] ? ds->cdp_id[x] < ds->cdp_id[y]
+                                            : x < y;
+    });
+    long long traces = ds->ntraces[g];
+    h.leg_gather.push_back(g);
+    h.leg_d2.push_back(0.0f);
+    h.leg_dm.push_back(0.0f);
+    for (int o : nb) {
+      const float dx = h.mx[o] - h.mx[g];
+      const float dy = h.my[o] - h.my[g];
+      h.leg_gather.push_back(o);
+      h.leg_d2.push_back(dx * dx + dy * dy);
+      h.leg_dm.push_back(dx);
+      traces += ds->ntraces[o];
+    }
+    h.leg_off.push_back(static_cast<int>(h.leg_gather.size()));
+    h.row_traces[r] = traces;
+  }
+  return h;
+}
+
+// ---------------------------------------------------------------------------
+// Device buffers.
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t n) {
+    if (n <= bytes && p) return;
+    if (p) VG_CUDA(cudaFree(p));
+    p = nullptr;
+    bytes = 0;
+    if (n == 0) n = 16;
+    VG_CUDA(cudaMalloc(&p, n));
+    bytes = n;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+enum BufId {
+  B_SAMPLES, B_H2, B_NTR, B_LEGOFF, B_LEGG, B_LEGD2, B_LEGDM, B_T0, B_A, B_B,
+  B_V, B_BIDX, B_BS, B_BST, B_MAT, B_VALID, B_COUNT
+};
+
+struct DeviceState {
+  int dev = 0;
+  cudaStream_t stream = nullptr, copy_stream = nullptr;
+  DevBuf bufs[B_COUNT];
+  std::vector<cudaEvent_t> events;
+  cudaEvent_t ev(size_t i) {
+    while (events.size() <= i) {
+      cudaEvent_t e;
+      VG_CUDA(cudaEventCreate(&e));
+      events.push_back(e);
+    }
+    return events[i];
+  }
+  void init(int d) {
+    dev = d;
+    VG_CUDA(cudaSetDevice(d));
+    VG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    VG_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+  }
+  void destroy() {
+    cudaSetDevice(dev);
+    for (auto& b : bufs) b.release();
+    for (auto e : events) cudaEventDestroy(e);
+    events.clear();
+    if (stream) cudaStreamDestroy(stream);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    stream = copy_stream = nullptr;
+  }
+};
+
+// A shard: rows [r0, r1) of the global sweep on one device.
+struct Shard {
+  int r0 = 0, r1 = 0;
+  std::vector<int> local_gathers;  // local -> global gather, ascending
+  std::vector<int> leg_off, leg_gather;
+  std::vector<float> leg_d2, leg_dm;
+  std::vector<float> h2;
+  std::vector<int> ntr;
+  std::vector<int> wave_rows;  // wave boundaries (local rows)
+  std::vector<int> wave_need;  // local gathers needed up to each wave
+  long long nominal = 0;
+};
+
+Shard make_shard(const HostSweep& h, const velan_gpu_dataset* ds, int r0,
+                 int r1, bool identity_gathers) {
+  Shard s;
+  s.r0 = r0;
+  s.r1 = r1;
+  const int lb = h.leg_off[r0], le = h.leg_off[r1];
+  if (identity_gathers) {
+    s.local_gathers.resize(h.G);
+    std::iota(s.local_gathers.begin(), s.local_gathers.end(), 0);
+  } else {
+    s.local_gathers.assign(h.leg_gather.begin() + lb, h.leg_gather.begin() + le);
+    std::sort(s.local_gathers.begin(), s.local_gathers.end());
+    s.local_gathers.erase(
+        std::unique(s.local_gathers.begin(), s.local_gathers.end()),
+        s.local_gathers.end());
+  }
+  std::vector<int> g2l;
+  if (!identity_gathers) {
+    g2l.assign(h.G, -1);
+    for (size_t i = 0; i < s.local_gathers.size(); ++i)
+      g2l[s.local_gathers[i]] = static_cast<int>(i);
+  }
+  const int L = static_cast<int>(s.local_gathers.size());
+  s.h2.resize(static_cast<size_t>(L) * h.M);
+  s.ntr.resize(L);
+  for (int l = 0; l < L; ++l) {
+    const int g = s.local_gathers[l];
+    std::memcpy(&s.h2[static_cast<size_t>(l) * h.M],
+                &h.h2[static_cast<size_t>(g) * h.M], sizeof(float) * h.M);
+    s.ntr[l] = ds->ntraces[g];
+  }
+  s.leg_off.resize(r1 - r0 + 1);
+  for (int r = r0; r <= r1; ++r) s.leg_off[r - r0] = h.leg_off[r] - lb;
+  s.leg_gather.resize(le - lb);
+  for (int i = lb; i < le; ++i)
+    s.leg_gather[i - lb] =
+        identity_gathers ? h.leg_gather[i] : g2l[h.leg_gather[i]];
+  s.leg_d2.assign(h.leg_d2.begin() + lb, h.leg_d2.begin() + le);
+  s.leg_dm.assign(h.leg_dm.begin() + lb, h.leg_dm.begin() + le);
+  for (int r = r0; r < r1; ++r)
+    s.nominal += h.row_traces[r] * static_cast<long long>(h.ns) * h.ncand;
+  // waves: ~equal nominal work, >= 2 waves of CTAs per launch when possible
+  const long long per_row_ctas = (h.ns + kThreads - 1) / kThreads;
+  const long long rows = r1 - r0;
+  long long total_work = 0;
+  for (int r = r0; r < r1; ++r) total_work += h.row_traces[r];
+  total_work *= static_cast<long long>(h.ns) * h.ncand * h.w;
+  // target ~1.5e12 window evaluations per launch (~1 s), but at least
+  // 8 waves worth of CTAs, and at most 65535 rows (grid.y)
+  const long long target_evals = 1500000000000LL;
+  long long rows_per_wave =
+      std::max<long long>(1, rows * target_evals / std::max(total_work, 1LL));
+  rows_per_wave = std::max<long long>(
+      rows_per_wave, std::min<long long>(rows, (148LL * 4 * 8) / per_row_ctas + 1));
+  rows_per_wave = std::min<long long>(rows_per_wave, 65535);
+  rows_per_wave = std::max<long long>(rows_per_wave, 1);
+  int need = 0;
+  for (long long b = 0; b < rows; b += rows_per_wave) {
+    const long long e = std::min(rows, b + rows_per_wave);
+    for (long long i = s.leg_off[b]; i < s.leg_off[e]; ++i)
+      need = std::max(need, s.leg_gather[i] + 1);
+    s.wave_rows.push_back(static_cast<int>(b));
+    s.wave_need.push_back(need);
+  }
+  s.wave_rows.push_back(static_cast<int>(rows));
+  return s;
+}
+
+template <class T>
+void upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
+  b.ensure(sizeof(T) * std::max<size_t>(v.size(), 1));
+  if (!v.empty())
+    VG_CUDA(cudaMemcpyAsync(b.p, v.data(), sizeof(T) * v.size(),
+                            cudaMemcpyHostToDevice, st));
+}
+
+void set_smem_attr(KernelFn fn, size_t smem) {
+  VG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+}
+
+int staging_cap(int ns) {
+  int cap = std::max(4096, ((ns + 3) / 4) * 4 + 8);
+  return (cap + 31) / 32 * 32;
+}
+
+struct RunOut {
+  uint64_t valid = 0;
+  double kernel_ms = 0.0;
+  int launches = 0;
+};
+
+// Run one shard on one device.  When out_host is true the result arrays are
+// host memory and rows are copied back at the end; samples are uploaded
+// from host (per wave) unless d_samples_ext is given.
+RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
+                 const velan_gpu_dataset* ds, const velan_gpu_scan* sc,
+                 velan_gpu_result* res, const float* d_samples_ext,
+                 cudaStream_t user_stream, bool tables_resident,
+                 bool samples_resident) {
+  VG_CUDA(cudaSetDevice(D.dev));
+  cudaStream_t st = user_stream ? user_stream : D.stream;
+  const int rows = s.r1 - s.r0;
+  RunOut out;
+  if (rows <= 0) return out;
+  const int L = static_cast<int>(s.local_gathers.size());
+  const size_t trace_floats = static_cast<size_t>(h.M) * h.ns;
+
+  if (!tables_resident) {
+    upload(D.bufs[B_H2], s.h2, st);
+    upload(D.bufs[B_NTR], s.ntr, st);
+    upload(D.bufs[B_LEGOFF], s.leg_off, st);
+    upload(D.bufs[B_LEGG], s.leg_gather, st);
+    upload(D.bufs[B_LEGD2], s.leg_d2, st);
+    upload(D.bufs[B_LEGDM], s.leg_dm, st);
+    upload(D.bufs[B_T0], h.t0, st);
+    upload(D.bufs[B_A], h.a, st);
+    upload(D.bufs[B_B], h.b, st);
+    upload(D.bufs[B_V], h.v, st);
+  }
+  const bool out_host = res->out_mem == VELAN_MEM_HOST;
+  const size_t cells = static_cast<size_t>(rows) * h.ns;
+  int32_t* d_bidx;
+  float *d_bs, *d_bst, *d_mat = nullptr;
+  if (out_host) {
+    D.bufs[B_BIDX].ensure(cells * 4);
+    D.bufs[B_BS].ensure(cells * 4);
+    D.bufs[B_BST].ensure(cells * 4);
+    d_bidx = D.bufs[B_BIDX].as<int32_t>();
+    d_bs = D.bufs[B_BS].as<float>();
+    d_bst = D.bufs[B_BST].as<float>();
+    if (res->matrix) {
+      D.bufs[B_MAT].ensure(cells * h.ncand * 4);
+      d_mat = D.bufs[B_MAT].as<float>();
+    }
+  } else {
+    d_bidx = res->best_idx + static_cast<size_t>(s.r0) * h.ns;
+    d_bs = res->best_semblance + static_cast<size_t>(s.r0) * h.ns;
+    d_bst = res->best_stack + static_cast<size_t>(s.r0) * h.ns;
+    if (res->matrix)
+      d_mat = res->matrix + static_cast<size_t>(s.r0) * h.ns * h.ncand;
+  }
+  D.bufs[B_VALID].ensure(8);
+  VG_CUDA(cudaMemsetAsync(D.bufs[B_VALID].p, 0, 8, st));
+
+  // samples: external device pointer, resident, or uploaded per wave
+  const float* d_samples = d_samples_ext;
+  const bool upload_samples = !d_samples_ext && !samples_resident;
+  if (!d_samples_ext) {
+    if (upload_samples) D.bufs[B_SAMPLES].ensure(
+        std::max<size_t>(1, static_cast<size_t>(L) * trace_floats * 4 + 64));
+    d_samples = D.bufs[B_SAMPLES].as<float>();
+  }
+
+  const KernelChoice kc = choose_kernel(h.op, sc->variant, h.w);
+  ScanParams p{};
+  p.samples = d_samples;
+  p.h2 = D.bufs[B_H2].as<float>();
+  p.ntr = D.bufs[B_NTR].as<int>();
+  p.leg_off = D.bufs[B_LEGOFF].as<int>();
+  p.leg_gather = D.bufs[B_LEGG].as<int>();
+  p.leg_d2 = D.bufs[B_LEGD2].as<float>();
+  p.leg_dm = D.bufs[B_LEGDM].as<float>();
+  p.t0 = D.bufs[B_T0].as<float>();
+  p.cand_a = D.bufs[B_A].as<float>();
+  p.cand_b = D.bufs[B_B].as<float>();
+  p.cand_v = D.bufs[B_V].as<float>();
+  p.n_a = h.n_a;
+  p.n_b = h.n_b;
+  p.n_c = h.n_c;
+  p.ncand = h.ncand;
+  p.Mmax = h.M;
+  p.ns = h.ns;
+  p.w = h.w;
+  p.vec4 = (h.ns % 4 == 0) &&
+           (reinterpret_cast<uintptr_t>(d_samples) % 16 == 0);
+  p.cap = staging_cap(h.ns);
+  p.dt = h.dt;
+  {
+    const double inv = 1.0 / h.dt;
+    p.inv_hi = static_cast<float>(inv);
+    p.inv_lo = static_cast<float>(inv - static_cast<double>(p.inv_hi));
+    p.amb_eps = static_cast<float>(std::ldexp(std::max(h.ns, 16), -40));
+  }
+  p.best_idx = d_bidx;
+  p.best_s = d_bs;
+  p.best_stack = d_bst;
+  p.matrix = d_mat;
+  p.valid = D.bufs[B_VALID].as<unsigned long long>();
+  const size_t smem = static_cast<size_t>(2) * p.cap * sizeof(float);
+  set_smem_attr(kc.fn, smem);
+
+  const int nwaves = static_cast<int>(s.wave_need.size());
+  int uploaded = 0;
+  for (int wv = 0; wv < nwaves; ++wv) {
+    if (upload_samples && s.wave_need[wv] > uploaded) {
+      // contiguous runs of global gathers -> one copy each
+      int l = uploaded;
+      const int need = s.wave_need[wv];
+      while (l < need) {
+        int e = l + 1;
+        while (e < need && s.local_gathers[e] == s.local_gathers[e - 1] + 1) ++e;
+        VG_CUDA(cudaMemcpyAsync(
+            D.bufs[B_SAMPLES].as<float>() + static_cast<size_t>(l) * trace_floats,
+            ds->samples + static_cast<size_t>(s.local_gathers[l]) * trace_floats,
+            sizeof(float) * trace_floats * (e - l), cudaMemcpyHostToDevice,
+            D.copy_stream));
+        l = e;
+      }
+      uploaded = need;
+      VG_CUDA(cudaEventRecord(D.ev(2 * nwaves + wv), D.copy_stream));
+      VG_CUDA(cudaStreamWaitEvent(st, D.ev(2 * nwaves + wv), 0));
+    }
+    const int rb = s.wave_rows[wv], re = s.wave_rows[wv + 1];
+    p.row_first = rb;
+    dim3 grid((h.ns + kThreads - 1) / kThreads, re - rb);
+    VG_CUDA(cudaEventRecord(D.ev(2 * wv), st));
+    kc.fn<<<grid, kThreads, smem, st>>>(p);
+    VG_CUDA(cudaGetLastError());
+    VG_CUDA(cudaEventRecord(D.ev(2 * wv + 1), st));
+    ++out.launches;
+  }
+  unsigned long long valid = 0;
+  VG_CUDA(cudaMemcpyAsync(&valid, D.bufs[B_VALID].p, 8, cudaMemcpyDeviceToHost,
+                          st));
+  if (out_host) {
+    VG_CUDA(cudaMemcpyAsync(res->best_idx + static_cast<size_t>(s.r0) * h.ns,
+                            d_bidx, cells * 4, cudaMemcpyDeviceToHost, st));
+    VG_CUDA(cudaMemcpyAsync(res->best_semblance + static_cast<size_t>(s.r0) * h.ns,
+                            d_bs, cells * 4, cudaMemcpyDeviceToHost, st));
+    VG_CUDA(cudaMemcpyAsync(res->best_stack + static_cast<size_t>(s.r0) * h.ns,
+                            d_bst, cells * 4, cudaMemcpyDeviceToHost, st));
+    if (res->matrix)
+      VG_CUDA(cudaMemcpyAsync(
+          res->matrix + static_cast<size_t>(s.r0) * h.ns * h.ncand, d_mat,
+          cells * h.ncand * 4, cudaMemcpyDeviceToHost, st));
+  }
+  VG_CUDA(cudaStreamSynchronize(st));
+  out.valid = valid;
+  for (int wv = 0; wv < nwaves; ++wv) {
+    float ms = 0.0f;
+    VG_CUDA(cudaEventElapsedTime(&ms, D.ev(2 * wv), D.ev(2 * wv + 1)));
+    out.kernel_ms += ms;
+  }
+  return out;
+}
+
+// Balanced contiguous row blocks by nominal work.
+std::vector<int> split_rows(const HostSweep& h, int parts) {
+  std::vector<int> cuts(1, 0);
+  long long total = 0;
+  for (int r = 0; r < h.rows; ++r) total += h.row_traces[r];
+  long long acc = 0;
+  int r = 0;
+  for (int p = 1; p < parts; ++p) {
+    const long long target = total * p / parts;
+    while (r < h.rows && acc + h.row_traces[r] <= target) acc += h.row_traces[r++];
+    cuts.push_back(r);
+  }
+  cuts.push_back(h.rows);
+  return cuts;
+}
+
+}  // namespace
+}  // namespace velan_gpu
+
+// ===========================================================================
+// C ABI
+
+using namespace velan_gpu;
+
+struct velan_gpu_ctx {
+  std::vector<DeviceState> devs;
+  std::mutex lock;
+};
+
+struct velan_gpu_plan {
+  velan_gpu_ctx* ctx = nullptr;
+  DeviceState dev;
+  HostSweep h;
+  Shard shard;
+  velan_gpu_dataset ds{};
+  velan_gpu_scan sc{};
+  const float* d_samples_ext = nullptr;
+  int launches = 0;
+};
+
+#define VG_API_BEGIN try {
+#define VG_API_END                                    \
+  }                                                   \
+  catch (const ApiError& e) {                         \
+    g_last_error = e.what();                          \
+    return e.code;                                    \
+  }                                                   \
+  catch (const std::exception& e) {                   \
+    g_last_error = e.what();                          \
+    return VELAN_GPU_ERUNTIME;                        \
+  }                                                   \
+  catch (...) {                                       \
+    g_last_error = "unknown error";                   \
+    return VELAN_GPU_ERUNTIME;                        \
+  }
+
+extern "C" {
+
+int velan_gpu_abi_version(void) { return VELAN_GPU_ABI_VERSION; }
+
+const char* velan_gpu_last_error(void) { return g_last_error.c_str(); }
+
+int velan_gpu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int ok = 0;
+  for (int d = 0; d < n; ++d) {
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, d) == cudaSuccess && prop.major == 10 &&
+        prop.minor == 0)
+      ++ok;
+  }
+  return ok;
+}
+
+int velan_gpu_create(const int32_t* device_ids, int32_t n_devices,
+                     velan_gpu_ctx** out) {
+  VG_API_BEGIN
+  if (!out) throw ApiError(VELAN_GPU_EPARAM, "out is null");
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw ApiError(VELAN_GPU_ENODEV, "no CUDA device visible");
+  }
+  if (n_devices < 1) throw ApiError(VELAN_GPU_EPARAM, "n_devices must be >= 1");
+  auto ctx = std::make_unique<velan_gpu_ctx>();
+  ctx->devs.resize(n_devices);
+  for (int i = 0; i < n_devices; ++i) {
+    const int d = device_ids ? device_ids[i] : i;
+    if (d < 0 || d >= n)
+      throw ApiError(VELAN_GPU_ENODEV, fmt("device %lld not visible", d));
+    cudaDeviceProp prop;
+    VG_CUDA(cudaGetDeviceProperties(&prop, d));
+    if (prop.major != 10 || prop.minor != 0)
+      throw ApiError(VELAN_GPU_ENODEV,
+                     fmt("device %lld is sm_%lld; kernels are built for "
+                         "sm_100a only",
+                         d, prop.major * 10 + prop.minor));
+    ctx->devs[i].init(d);
+  }
+  *out = ctx.release();
+  return VELAN_GPU_OK;
+  VG_API_END
+}
+
+void velan_gpu_destroy(velan_gpu_ctx* ctx) {
+  if (!ctx) return;
+  for (auto& d : ctx->devs) d.destroy();
+  delete ctx;
+}
+
+int velan_gpu_validate(const velan_gpu_dataset* ds, const velan_gpu_scan* sc) {
+  VG_API_BEGIN
+  validate(ds, sc, sc && sc->op != VELAN_OP_NMO);
+  return VELAN_GPU_OK;
+  VG_API_END
+}
+
+static int run_oneshot(velan_gpu_ctx* ctx, const velan_gpu_dataset* ds,
+                       const velan_gpu_scan* sc, velan_gpu_result* res,
+                       bool crs) {
+  VG_API_BEGIN
+  const auto t_start = std::chrono::steady_clock::now();
+  if (!ctx || !res) throw ApiError(VELAN_GPU_EPARAM, "null context or result");
+  validate(ds, sc, crs);
+  res->valid_intersections = 0;
+  res->nominal_intersections = 0;
+  res->kernel_ms = 0.0;
+  if (ds->n_gathers == 0) {
+    res->total_ms = 0.0;
+    return VELAN_GPU_OK;
+  }
+  if (!res->best_idx || !res->best_semblance || !res->best_stack)
+    throw ApiError(VELAN_GPU_EPARAM, "result arrays are null");
+  if (ds->samples_mem == VELAN_MEM_DEVICE && ctx->devs.size() != 1)
+    throw ApiError(VELAN_GPU_ECONFIG,
+                   "device-resident samples need a single-device context");
+  if (res->out_mem == VELAN_MEM_DEVICE && ctx->devs.size() != 1)
+    throw ApiError(VELAN_GPU_ECONFIG,
+                   "device-resident outputs need a single-device context");
+  std::lock_guard<std::mutex> guard(ctx->lock);
+  const HostSweep h = build_sweep(ds, sc);
+  const int nd = static_cast<int>(ctx->devs.size());
+  const std::vector<int> cuts = split_rows(h, nd);
+  std::vector<RunOut> outs(nd);
+  std::vector<std::string> errs(nd);
+  std::vector<int> codes(nd, 0);
+  const bool dev_samples = ds->samples_mem == VELAN_MEM_DEVICE;
+  auto body = [&](int i) {
+    try {
+      const Shard s = make_shard(h, ds, cuts[i], cuts[i + 1], dev_samples);
+      outs[i] = run_shard(ctx->devs[i], h, s, ds, sc, res,
+                          dev_samples ? ds->samples : nullptr, nullptr, false,
+                          false);
+    } catch (const ApiError& e) {
+      codes[i] = e.code;
+      errs[i] = e.what();
+    } catch (const std::exception& e) {
+      codes[i] = VELAN_GPU_ERUNTIME;
+      errs[i] = e.what();
+    }
+  };
+  if (nd == 1) {
+    body(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int i = 0; i < nd; ++i) th.emplace_back(body, i);
+    for (auto& t : th) t.join();
+  }
+  for (int i = 0; i < nd; ++i)
+    if (codes[i]) throw ApiError(codes[i], errs[i]);
+  uint64_t valid = 0;
+  double kms = 0.0;
+  for (auto& o : outs) {
+    valid += o.valid;
+    kms = std::max(kms, o.kernel_ms);
+  }
+  uint64_t nominal = 0;
+  for (int r = 0; r < h.rows; ++r)
+    nominal += static_cast<uint64_t>(h.row_traces[r]) * h.ns * h.ncand;
+  if (res->row_gather)
+    for (int r = 0; r < h.rows; ++r) res->row_gather[r] = h.row_gather[r];
+  res->valid_intersections = valid;
+  res->nominal_intersections = nominal;
+  res->kernel_ms = kms;
+  res->total_ms = std::chrono::duration<double, std::milli>(
+                      std::chrono::steady_clock::now() - t_start)
+                      .count();
+  return VELAN_GPU_OK;
+  VG_API_END
+}
+
+int velan_gpu_cmp(velan_gpu_ctx* ctx, const velan_gpu_dataset* ds,
+                  const velan_gpu_scan* sc, velan_gpu_result* res) {
+  return run_oneshot(ctx, ds, sc, res, false);
+}
+
+int velan_gpu_crs(velan_gpu_ctx* ctx, const velan_gpu_dataset* ds,
+                  const velan_gpu_scan* sc, velan_gpu_result* res) {
+  return run_oneshot(ctx, ds, sc, res, true);
+}
+
+int velan_gpu_plan_create(velan_gpu_ctx* ctx, const velan_gpu_dataset* ds,
+                          const velan_gpu_scan* sc, velan_gpu_plan** out) {
+  VG_API_BEGIN
+  if (!ctx || !out) throw ApiError(VELAN_GPU_EPARAM, "null context or out");
+  *out = nullptr;
+  validate(ds, sc, sc && sc->op != VELAN_OP_NMO);
+  if (ctx->devs.size() != 1)
+    throw ApiError(VELAN_GPU_ECONFIG, "plans need a single-device context");
+  auto plan = std::make_unique<velan_gpu_plan>();
+  plan->ctx = ctx;
+  plan->ds = *ds;
+  plan->sc = *sc;
+  plan->dev.init(ctx->devs[0].dev);
+  plan->h = build_sweep(ds, sc);
+  const bool dev_samples = ds->samples_mem == VELAN_MEM_DEVICE;
+  plan->shard = make_shard(plan->h, ds, 0, plan->h.rows, dev_samples);
+  plan->d_samples_ext = dev_samples ? ds->samples : nullptr;
+  if (ds->n_gathers > 0) {
+    // resident tables + samples: one upload now, none per execute
+    DeviceState& D = plan->dev;
+    const Shard& s = plan->shard;
+    const HostSweep& h = plan->h;
+    upload(D.bufs[B_H2], s.h2, D.stream);
+    upload(D.bufs[B_NTR], s.ntr, D.stream);
+    upload(D.bufs[B_LEGOFF], s.leg_off, D.stream);
+    upload(D.bufs[B_LEGG], s.leg_gather, D.stream);
+    upload(D.bufs[B_LEGD2], s.leg_d2, D.stream);
+    upload(D.bufs[B_LEGDM], s.leg_dm, D.stream);
+    upload(D.bufs[B_T0], h.t0, D.stream);
+    upload(D.bufs[B_A], h.a, D.stream);
+    upload(D.bufs[B_B], h.b, D.stream);
+    upload(D.bufs[B_V], h.v, D.stream);
+    if (!dev_samples) {
+      const size_t tf = static_cast<size_t>(h.M) * h.ns;
+      const size_t L = s.local_gathers.size();
+      D.bufs[B_SAMPLES].ensure(L * tf * 4 + 64);
+      for (size_t l = 0; l < L; ++l)
+        VG_CUDA(cudaMemcpyAsync(D.bufs[B_SAMPLES].as<float>() + l * tf,
+                                ds->samples + static_cast<size_t>(s.local_gathers[l]) * tf,
+                                tf * 4, cudaMemcpyHostToDevice, D.stream));
+    }
+    VG_CUDA(cudaStreamSynchronize(D.stream));
+  }
+  plan->ds.samples = nullptr;  // host pointers are not retained
+  plan->ds.coords = nullptr;
+  plan->ds.ntraces = nullptr;
+  plan->ds.cdp_id = nullptr;
+  plan->sc.a = plan->sc.b = plan->sc.v = nullptr;
+  *out = plan.release();
+  return VELAN_GPU_OK;
+  VG_API_END
+}
+
+int velan_gpu_plan_execute(velan_gpu_plan* plan, velan_gpu_result* res,
+                           void* stream) {
+  VG_API_BEGIN
+  const auto t_start = std::chrono::steady_clock::now();
+  if (!plan || !res) throw ApiError(VELAN_GPU_EPARAM, "null plan or result");
+  res->valid_intersections = 0;
+  res->nominal_intersections = 0;
+  res->kernel_ms = 0.0;
+  if (plan->h.rows == 0) return VELAN_GPU_OK;
+  if (!res->best_idx || !res->best_semblance || !res->best_stack)
+    throw ApiError(VELAN_GPU_EPARAM, "result arrays are null");
+  const RunOut o =
+      run_shard(plan->dev, plan->h, plan->shard, &plan->ds, &plan->sc, res,
+                plan->d_samples_ext, static_cast<cudaStream_t>(stream), true,
+                plan->d_samples_ext == nullptr);
+  plan->launches = o.launches;
+  if (res->row_gather)
+    for (int r = 0; r < plan->h.rows; ++r) res->row_gather[r] = plan->h.row_gather[r];
+  res->valid_intersections = o.valid;
+  res->nominal_intersections = static_cast<uint64_t>(plan->shard.nominal);
+  res->kernel_ms = o.kernel_ms;
+  res->total_ms = std::chrono::duration<double, std::milli>(
+                      std::chrono::steady_clock::now() - t_start)
+                      .count();
+  return VELAN_GPU_OK;
+  VG_API_END
+}
+
+int velan_gpu_plan_launches(const velan_gpu_plan* plan) {
+  if (!plan) return 0;
+  return static_cast<int>(plan->shard.wave_need.size());
+}
+
+void velan_gpu_plan_destroy(velan_gpu_plan* plan) {
+  if (!plan) return;
+  plan->dev.destroy();
+  delete plan;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// hit_for test hook
+
+namespace velan_gpu {
+namespace {
+__global__ void hit_batch_kernel(const float* t, int n, double dt, int ns,
+                                 int w, int variant, float inv_hi,
+                                 float inv_lo, float amb_eps, int32_t* k1,
+                                 float* x, uint8_t* valid) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int kk;
+  float xx;
+  bool vv;
+  if (variant == VELAN_VARIANT_EXACT) {
+    hit_exact(t[i], dt, ns, w, kk, xx, vv);
+  } else {
+    ScanParams p{};
+    p.dt = dt;
+    p.ns = ns;
+    p.inv_hi = inv_hi;
+    p.inv_lo = inv_lo;
+    p.amb_eps = amb_eps;
+    hit_fast(t[i], p, w, kk, xx, vv);
+  }
+  // the reference reports k1 even for invalid hits; recompute it exactly
+  const double base = floor(__ddiv_rn(static_cast<double>(t[i]), dt));
+  const bool in_range = base >= -2147483648.0 && base < 2147483648.0;
+  k1[i] = in_range ? static_cast<int>(base) - (w >> 1)
+                   : static_cast<int>(0x80000000u) - (w >> 1);
+  if (vv) k1[i] = kk;
+  x[i] = xx;
+  valid[i] = vv ? 1 : 0;
+}
+}  // namespace
+}  // namespace velan_gpu
+
+extern "C" int velan_gpu_hit_batch(const float* t, int32_t n, double dt_s,
+                                   int32_t ns, int32_t w, int32_t variant,
+                                   int32_t* k1, float* x, uint8_t* valid) {
+  VG_API_BEGIN
+  if (n < 0 || (n > 0 && (!t || !k1 || !x || !valid)))
+    throw ApiError(VELAN_GPU_EPARAM, "bad arguments");
+  if (velan_gpu_device_count() == 0)
+    throw ApiError(VELAN_GPU_ENODEV, "no sm_100 device visible");
+  if (n == 0) return VELAN_GPU_OK;
+  float* dt_ = nullptr;
+  int32_t* dk = nullptr;
+  float* dx = nullptr;
+  uint8_t* dv = nullptr;
+  VG_CUDA(cudaMalloc(&dt_, n * 4));
+  VG_CUDA(cudaMalloc(&dk, n * 4));
+  VG_CUDA(cudaMalloc(&dx, n * 4));
+  VG_CUDA(cudaMalloc(&dv, n));
+  VG_CUDA(cudaMemcpy(dt_, t, n * 4, cudaMemcpyHostToDevice));
+  const double inv = 1.0 / dt_s;
+  const float hi = static_cast<float>(inv);
+  const float lo = static_cast<float>(inv - hi);
+  const float eps = static_cast<float>(std::ldexp(std::max(ns, 16), -40));
+  hit_batch_kernel<<<(n + 255) / 256, 256>>>(dt_, n, dt_s, ns, w, variant, hi,
+                                             lo, eps, dk, dx, dv);
+  VG_CUDA(cudaGetLastError());
+  VG_CUDA(cudaMemcpy(k1, dk, n * 4, cudaMemcpyDeviceToHost));
+  VG_CUDA(cudaMemcpy(x, dx, n * 4, cudaMemcpyDeviceToHost));
+  VG_CUDA(cudaMemcpy(valid, dv, n, cudaMemcpyDeviceToHost));
+  cudaFree(dt_);
+  cudaFree(dk);
+  cudaFree(dx);
+  cudaFree(dv);
+  return VELAN_GPU_OK;
+  VG_API_END
+}
