@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""bench.py — BASELINE.json metric: semblance evals/s of the CMP/CRS parameter
+search on N B200s, with the FP32 roofline fraction and the host-CPU reference.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cmp_large|cmp_small|crs_small|crs_large]
+
+A "step" is one pass of the scan over one rank's workload: the BASELINE
+configuration itself (default configs[1], CMP large: 8192 gathers x 60 traces
+x 2000 samples, 401 candidates, w = 15).  Multi-GPU is weak scaling: every
+rank scans its own contiguous block of a longer line (no collective on the
+data path; only a barrier and the max-over-ranks timing reduction).
+
+One JSON line on rank 0.  ``value`` = nominal evals (midpoints x t0 x
+candidates x traces x w, BASELINE's unit) of all ranks / the max over ranks of
+the device time of K steps with the input resident in HBM (3.9 GB per GPU,
+larger than the 126 MB L2, so no flush is needed).  ``e2e`` = the same metric
+through the one-shot C-ABI call velan_gpu_cmp/crs from pinned host buffers
+(H2D of the samples and D2H of the picks inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "semblance evals/sec"
+UNIT = "evals/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="cmp_large")
+    ap.add_argument("--variant", default="fast", choices=["fast", "exact"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="target CPU time of the cpu_baseline sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md clocks line)
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.gpu)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        sms, maxes, power, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sms.append(float(f[1]))
+                maxes.append(float(f[2]))
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sms:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sms.sort()
+        return {"sm_mhz": sms[len(sms) // 2], "sm_max_mhz": max(maxes),
+                "reasons": sorted(reasons), "samples": len(sms),
+                "power_w_max": max(power) if power else None}
+
+
+def physical_gpu(local: int) -> int:
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        parts = [p for p in vis.split(",") if p.strip()]
+        if local < len(parts) and parts[local].strip().isdigit():
+            return int(parts[local])
+    return local
+
+
+# ---------------------------------------------------------------------------
+
+def algorithmic_flops(valid: int, nominal: int, w: int) -> float:
+    """12 + 7w flops per valid intersection, 12 per out-of-range one
+    (bench.hpp:47-51)."""
+    return valid * (12.0 + 7.0 * w) + (nominal - valid) * 12.0
+
+
+def load_traffic(workload: str):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(workload)
+    except Exception:
+        return None
+
+
+def cpu_reference_sample(wl, ds, seconds: float, threads: int):
+    """Time the UNMODIFIED reference kernels (oracle/_ref: velan's blocked
+    scan_tile_blocked driven like scan_sweep, parallel_for_indexed over all
+    host threads) on a bounded gather sample of the same workload.  Falls
+    back to the C restatement (kind "port") if _ref was not built."""
+    import numpy as np
+
+    import oracle
+    G = ds.ncdps
+    kind = "reference" if oracle.ref_available() else "port"
+    ns = ds.ns
+    ks_all = np.arange(ns, dtype=np.int32)
+
+    def run(n_rows):
+        rows = np.repeat(np.arange(n_rows, dtype=np.int32), ns)
+        ks = np.tile(ks_all, n_rows)
+        t = time.perf_counter()
+        if wl.op == "nmo" and kind == "reference":
+            r = oracle.ref_run_cells(ds, "nmo", wl.config.w, wl.config.grid(), rows, ks,
+                                     variant=1, workers=threads)
+        else:
+            r = oracle.run_cells(ds, wl.op, wl.config.w, wl.config.grid(), rows, ks,
+                                 apm=wl.apm, abc=wl.abc, threads=threads)
+        return time.perf_counter() - t, r
+
+    n0 = max(1, min(G, threads))
+    dt0, _ = run(n0)
+    n = int(min(G, max(n0, n0 * math.ceil(seconds / max(dt0, 1e-3)))))
+    n = max(n0, (n // n0) * n0)
+    dt, r = run(n)
+    tps = wl.traces_per_sweep()[:n]
+    evals = int(tps.sum()) * ns * wl.ncand * wl.config.w
+    return {"value": evals / dt, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{n} of {G} midpoints x {ns} t0 x {wl.ncand} candidates "
+                      f"(all traces, w={wl.config.w}), {dt:.2f} s",
+            "valid_evals_per_s": r.valid * wl.config.w / dt}
+
+
+# ---------------------------------------------------------------------------
+
+def run_reference_arm(args):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref)
+    on the host cores, same workload/metric; rank 0 only."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1907_11678_b200 import configs
+    wl = configs.WORKLOADS[args.workload]()
+    threads = os.cpu_count() or 1
+    # a gather sample of the same workload, generated like ours
+    n = max(threads, 8)
+    ds = wl.spec.generate(count=min(wl.spec.n_gathers, n * 16))
+    per_step = max(2.0, 60.0 / max(args.steps + args.warmup, 1))
+    for _ in range(args.warmup):
+        cpu_reference_sample(wl, ds, per_step, threads)
+    vals = []
+    last = None
+    for _ in range(args.steps):
+        last = cpu_reference_sample(wl, ds, per_step, threads)
+        vals.append(last["value"])
+    value = sorted(vals)[len(vals) // 2]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wl.name, "sample": last["sample"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads,
+                         "kind": last["kind"], "sample": last["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    import numpy as np
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+
+    from paper_1907_11678_b200 import Dataset, Engine, _native, configs
+    wl = configs.WORKLOADS[args.workload]()
+    wl.config.kernel_variant = args.variant
+    G = wl.spec.n_gathers
+    # weak scaling: rank r scans gathers [r*G, (r+1)*G) of a world*G line
+    t_gen = time.perf_counter()
+    ds = wl.spec.generate(first=rank * G, count=G, n_line=G * world)
+    t_gen = time.perf_counter() - t_gen
+    w = wl.config.w
+
+    eng = Engine([local])
+    # ---- device-resident value -------------------------------------------
+    samples_dev = torch.from_numpy(ds.samples).to(f"cuda:{local}")
+    dsd = Dataset(samples_dev, ds.coords, ds.ntraces, ds.cdp_id, ds.dt_us)
+    plan = eng.plan(dsd, wl.config, op=wl.op, apm=wl.apm, abc=wl.abc)
+    ns = ds.ns
+    bi = torch.empty((G, ns), dtype=torch.int32, device=f"cuda:{local}")
+    bs = torch.empty((G, ns), dtype=torch.float32, device=f"cuda:{local}")
+    bst = torch.empty((G, ns), dtype=torch.float32, device=f"cuda:{local}")
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        res = plan.execute(bi, bs, bst, stream=stream)
+    valid, nominal = int(res.valid_intersections), int(res.nominal_intersections)
+
+    def barrier():
+        if pg is not None:
+            pg.barrier()
+        torch.cuda.synchronize()
+
+    clocks = ClockSampler(physical_gpu(local))
+    barrier()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    kernel_ms = 0.0
+    e0.record(stream)
+    for _ in range(args.steps):
+        res = plan.execute(bi, bs, bst, stream=stream)
+        kernel_ms += res.kernel_ms
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    launches = plan.launches() * args.steps
+
+    evals_rank = nominal * w * args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    tot = torch.tensor([float(evals_rank), float(valid * w * args.steps)],
+                       dtype=torch.float64, device=f"cuda:{local}")
+    if pg is not None:
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        pg.all_reduce(tot, op=pg.ReduceOp.SUM)
+    ms_max = float(t.item())
+    evals_all, valid_all = float(tot[0].item()), float(tot[1].item())
+    value = evals_all / (ms_max * 1e-3)
+
+    # roofline of the dominant (only) kernel: algorithmic FP32 flops per
+    # launch / average launch duration (CUDA events on the launch stream)
+    flops_step = algorithmic_flops(valid, nominal, w)
+    achieved_tf = flops_step * args.steps / (kernel_ms * 1e-3) / 1e12
+    nsm = torch.cuda.get_device_properties(local).multi_processor_count
+    nominal_peak = 2.0 * 128 * nsm * 1965e6 / 1e12
+    import ctypes as C
+    pm = C.c_double(0.0)
+    _native.load().velan_gpu_measure_fp32_peak(local, C.byref(pm))
+    traffic = load_traffic(wl.name)
+
+    # ---- e2e through the one-shot C-ABI with pinned host buffers ----------
+    e2e = None
+    if not args.no_e2e:
+        pinned = torch.from_numpy(ds.samples).pin_memory()
+        dsh = Dataset(pinned, ds.coords, ds.ntraces, ds.cdp_id, ds.dt_us)
+        obi = torch.empty((G, ns), dtype=torch.int32).pin_memory()
+        obs = torch.empty((G, ns), dtype=torch.float32).pin_memory()
+        obst = torch.empty((G, ns), dtype=torch.float32).pin_memory()
+        run = (lambda: eng.run_cmp(dsh, wl.config, out=(obi, obs, obst))) if wl.op == "nmo" \
+            else (lambda: eng.run_crs(dsh, wl.config, wl.apm, wl.abc, out=(obi, obs, obst)))
+        run()  # warm-up (allocations cached in the context)
+        k_e2e = max(1, min(args.steps, 3))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            r = run()
+        barrier()
+        e2e_s = (time.perf_counter() - t0) / k_e2e
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+        if pg is not None:
+            pg.all_reduce(te, op=pg.ReduceOp.MAX)
+        e2e_s = float(te.item())
+        h2d = ds.samples.nbytes + ds.ntraces.nbytes + G * ds.fold * 4 + 4 * ns
+        d2h = 3 * 4 * G * ns
+        e2e = {"value": (evals_all / args.steps) / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": e2e_s * 1e3, "api": f"velan_gpu_{'cmp' if wl.op == 'nmo' else 'crs'}"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_reference_sample(wl, ds, args.cpu_seconds, os.cpu_count() or 1)
+        except Exception as ex:  # reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "unavailable",
+                   "sample": f"error: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (seeded generator, BASELINE.json shapes)",
+            "config": {"workload": wl.name, "midpoints_per_gpu": G, "traces": wl.spec.n_traces,
+                       "ns": ns, "dt_us": wl.spec.dt_us, "candidates": wl.ncand, "w": w,
+                       "operator": wl.op, "variant": args.variant,
+                       "l2": "input 3.9 GB/GPU > 126 MB L2 (no flush needed)"
+                       if wl.name.startswith("cmp_large") else "see DESIGN.md",
+                       "parallelism": f"dp{world} (contiguous midpoint blocks)"},
+            "valid_evals_per_s": valid_all / (ms_max * 1e-3),
+            "roofline": {"bound": "fp32", "achieved": achieved_tf, "peak": nominal_peak,
+                         "unit": "TFLOP/s", "frac": achieved_tf / nominal_peak,
+                         "traffic": traffic,
+                         "peak_source": "nominal FP32 FMA peak 2 x 128 x SMs x 1965 MHz "
+                                        "(MEASURED_PEAKS.json has no FP32 figure)",
+                         "measured_fma_peak": pm.value,
+                         "frac_of_measured_fma": achieved_tf / pm.value if pm.value else None,
+                         "flops_per_step": flops_step,
+                         "kernel_ms_per_step": kernel_ms / args.steps,
+                         "launches_per_step": plan.launches()},
+            "clocks": clk,
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gen_s": t_gen,
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    eng.close()
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -180,6 +180,10 @@ int velan_gpu_hit_batch(const float* t, int32_t n, double dt_s, int32_t ns,
  * (dipping curved reflectors).  Fills caller buffers shaped like
  * velan_gpu_dataset (samples [G][M][ns], coords [G][M][4], ntraces,
  * cdp_id).  See DESIGN.md §6 for the event model. */
+/* FP32 FMA throughput of `device` in TFLOP/s (best of 5 probes): the
+ * measured denominator of the FP32 roofline fraction (bench.py). */
+int velan_gpu_measure_fp32_peak(int32_t device, double* tflops);
+
 typedef struct velan_gpu_synth {
   int32_t kind;
   int32_t n_gathers, n_traces, ns;

@@ -113,6 +113,7 @@ SIGNATURES = {
     "velan_gpu_plan_destroy": (None, [_P]),
     "velan_gpu_hit_batch": (C.c_int, [_P, C.c_int32, C.c_double, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P]),
     "velan_gpu_synth_generate": (C.c_int, [C.POINTER(Synth), _P, _P, _P, _P]),
+    "velan_gpu_measure_fp32_peak": (C.c_int, [C.c_int32, C.POINTER(C.c_double)]),
 }
 
 _lib = None

@@ -337,7 +337,7 @@ class Engine:
 
     def _run(self, fn, ds: Dataset, op: int, variant: str, w: int,
              v: np.ndarray, abc: Optional[CrsAbcGrid], apm: float,
-             emit_matrix: bool) -> ScanResult:
+             emit_matrix: bool, out=None) -> ScanResult:
         lib = N.load()
         keep: list = []
         sc = _scan_struct(op, variant, w, v, abc, apm, keep)
@@ -345,9 +345,12 @@ class Engine:
         G = ds.ncdps
         ns = dss.ns
         ncand = abc.ncand if abc is not None else len(v)
-        best_idx = np.zeros((G, ns), np.int32)
-        best_s = np.zeros((G, ns), np.float32)
-        best_st = np.zeros((G, ns), np.float32)
+        if out is not None:  # caller-provided host buffers (e.g. pinned)
+            best_idx, best_s, best_st = out
+        else:
+            best_idx = np.zeros((G, ns), np.int32)
+            best_s = np.zeros((G, ns), np.float32)
+            best_st = np.zeros((G, ns), np.float32)
         rows = np.zeros(G, np.int32)
         mat = np.zeros((G, ns, ncand), np.float32) if emit_matrix else None
         res = N.Result()
@@ -362,6 +365,8 @@ class Engine:
         cands = abc.v if abc is not None else np.ascontiguousarray(v, np.float32)
         if G == 0:
             rows = np.zeros(0, np.int32)
+        if out is not None:
+            best_idx, best_s, best_st = (np.asarray(x) for x in out)
         return ScanResult(best_idx, best_s, best_st, cands, rows,
                           ds.cdp_id[rows] if G else ds.cdp_id, mat,
                           CacheStats(int(res.valid_intersections),
@@ -369,19 +374,19 @@ class Engine:
                           float(res.kernel_ms), float(res.total_ms))
 
     def run_cmp(self, ds: Dataset, config: ScanConfig,
-                emit_matrix: bool = False) -> ScanResult:
+                emit_matrix: bool = False, out=None) -> ScanResult:
         config.validate()
         return self._run(N.load().velan_gpu_cmp, ds, N.OP_NMO,
                          config.kernel_variant, config.w, config.grid(), None,
-                         0.0, emit_matrix)
+                         0.0, emit_matrix, out)
 
     def run_crs(self, ds: Dataset, config: ScanConfig, apm: float,
                 abc: Optional[CrsAbcGrid] = None,
-                emit_matrix: bool = False) -> ScanResult:
+                emit_matrix: bool = False, out=None) -> ScanResult:
         config.validate()
         op = N.OP_CRS_ABC if abc is not None else N.OP_CRS_D2
         return self._run(N.load().velan_gpu_crs, ds, op, config.kernel_variant,
-                         config.w, config.grid(), abc, apm, emit_matrix)
+                         config.w, config.grid(), abc, apm, emit_matrix, out)
 
     def plan(self, ds: Dataset, config: ScanConfig, op: str = "nmo",
              apm: float = 0.0, abc: Optional[CrsAbcGrid] = None) -> "Plan":

@@ -1,0 +1,175 @@
+"""GPU parity: the sm_100a kernels through the C-ABI against the CPU oracle.
+
+EXACT variant: bitwise equal to the reference arithmetic (semblance matrix,
+picks, stack, valid-intersection count).  FAST variant: identical picks except
+near-ties, semblance and stack within the north-star tolerance (1e-4 relative;
+stack with an absolute floor).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1907_11678_b200 import (CrsAbcGrid, ScanConfig, configs,
+                                    slowness_grid, velocity_grid)
+
+pytestmark = pytest.mark.gpu
+
+SEM_RTOL = 1e-4
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def assert_bitwise(gpu, ref_cells, ns, ncand=None):
+    G = gpu.best_idx.shape[0]
+    np.testing.assert_array_equal(gpu.best_idx.reshape(-1), ref_cells.best_idx)
+    np.testing.assert_array_equal(bits(gpu.best_semblance).reshape(-1),
+                                  bits(ref_cells.best_semblance))
+    np.testing.assert_array_equal(bits(gpu.stack_trace).reshape(-1),
+                                  bits(ref_cells.best_stack))
+    if ncand is not None and ref_cells.matrix is not None:
+        np.testing.assert_array_equal(bits(gpu.values).reshape(G * ns, ncand),
+                                      bits(ref_cells.matrix))
+    assert gpu.stats.naive_fetches == ref_cells.valid
+
+
+def assert_close(gpu, ref_cells, ns, ncand, stack_floor):
+    G = gpu.best_idx.shape[0]
+    m_gpu = gpu.values.reshape(G * ns, ncand)
+    rep = oracle.compare(m_gpu, ref_cells.matrix)
+    assert rep["max_rel_err"] <= SEM_RTOL, rep
+    assert rep["argmax_mismatches"] == 0, rep
+    same = gpu.best_idx.reshape(-1) == ref_cells.best_idx
+    # stack at the pick: relative with an absolute floor (near-cancelling mean)
+    d = np.abs(gpu.stack_trace.reshape(-1)[same] - ref_cells.best_stack[same])
+    tol = SEM_RTOL * np.abs(ref_cells.best_stack[same]) + stack_floor
+    assert np.all(d <= tol), float(np.max(d - tol))
+    assert gpu.stats.naive_fetches == ref_cells.valid
+
+
+@pytest.fixture(scope="module")
+def cmp_small():
+    w = configs.cmp_small()
+    return w, w.spec.generate()
+
+
+@pytest.mark.parametrize("variant", ["exact", "fast"])
+def test_cmp_small_full(engine, cmp_small, variant):
+    w, ds = cmp_small
+    cfg = ScanConfig(w=w.config.w, velocities=w.config.grid(), kernel_variant=variant)
+    r = engine.run_cmp(ds, cfg, emit_matrix=True)
+    rows, ks = oracle.all_cells(ds.ncdps, ds.ns)
+    ref = oracle.run_cells(ds, "nmo", cfg.w, cfg.grid(), rows, ks, matrix=True)
+    if variant == "exact":
+        assert_bitwise(r, ref, ds.ns, len(cfg.grid()))
+    else:
+        assert_close(r, ref, ds.ns, len(cfg.grid()), 1e-6 * float(np.abs(ds.samples).max()))
+    assert r.stats.nominal_intersections == ds.ncdps * ds.ns * 101 * 24
+
+
+@pytest.mark.parametrize("variant", ["exact", "fast"])
+def test_crs_d2_subset(engine, variant):
+    w = configs.crs_small()
+    ds = w.spec.generate(count=24)
+    v = velocity_grid(1500.0, 3500.0, 21)
+    cfg = ScanConfig(w=11, velocities=v, kernel_variant=variant)
+    r = engine.run_crs(ds, cfg, 125.0, emit_matrix=True)
+    rows, ks = oracle.all_cells(ds.ncdps, ds.ns)
+    ref = oracle.run_cells(ds, "d2", 11, v, rows, ks, apm=125.0, matrix=True)
+    if variant == "exact":
+        assert_bitwise(r, ref, ds.ns, 21)
+    else:
+        assert_close(r, ref, ds.ns, 21, 1e-6 * float(np.abs(ds.samples).max()))
+
+
+@pytest.mark.parametrize("variant", ["exact", "fast"])
+def test_crs_abc_subset(engine, variant):
+    w = configs.crs_small()
+    ds = w.spec.generate(count=16)
+    grid = CrsAbcGrid(np.linspace(-2e-4, 2e-4, 3), np.linspace(0, 1e-7, 3),
+                      np.linspace(1500, 3500, 7))
+    cfg = ScanConfig(w=11, velocities=grid.v, kernel_variant=variant)
+    r = engine.run_crs(ds, cfg, 125.0, abc=grid, emit_matrix=True)
+    rows, ks = oracle.all_cells(ds.ncdps, ds.ns)
+    ref = oracle.run_cells(ds, "abc", 11, None, rows, ks, apm=125.0, abc=grid, matrix=True)
+    if variant == "exact":
+        assert_bitwise(r, ref, ds.ns, grid.ncand)
+    else:
+        assert_close(r, ref, ds.ns, grid.ncand, 1e-6 * float(np.abs(ds.samples).max()))
+
+
+@pytest.mark.parametrize("w", [1, 2, 3, 4, 5, 8, 11, 13, 15, 16, 21, 32])
+def test_window_lengths_exact(engine, w):
+    rng = np.random.default_rng(100 + w)
+    G, M, ns = 3, 7, 131  # ns % 4 != 0: synchronous staging path
+    samples = rng.uniform(-1, 1, (G, M, ns)).astype(np.float32)
+    coords = np.zeros((G, M, 4), np.float32)
+    coords[:, :, 2] = np.linspace(0, 40, M)[None, :]
+    from paper_1907_11678_b200 import Dataset
+    ds = Dataset(samples, coords, np.full(G, M, np.int32), np.arange(G, dtype=np.uint32), 244)
+    v = velocity_grid(2000.0, 3000.0, 9)
+    cfg = ScanConfig(w=w, velocities=v)
+    if ns <= w + 1:
+        pytest.skip("window does not fit")
+    r = engine.run_cmp(ds, cfg, emit_matrix=True)
+    rows, ks = oracle.all_cells(G, ns)
+    ref = oracle.run_cells(ds, "nmo", w, v, rows, ks, matrix=True)
+    assert_bitwise(r, ref, ns, len(v))
+
+
+def test_hit_exact_matches_reference_rule():
+    from paper_1907_11678_b200 import _native as N
+    import ctypes as C
+    rng = np.random.default_rng(7)
+    dt = 0.004
+    ns, w = 1000, 11
+    k = rng.integers(0, ns, 20000)
+    t = np.concatenate([
+        (k * dt).astype(np.float32),                      # on-sample t0 values
+        rng.uniform(0, ns * dt, 20000).astype(np.float32),
+        np.array([0.0, 1e-30, np.inf, np.nan, -1.0, 1e9], np.float32)])
+    for variant in (0, 1):
+        k1 = np.zeros(len(t), np.int32)
+        x = np.zeros(len(t), np.float32)
+        valid = np.zeros(len(t), np.uint8)
+        code = N.load().velan_gpu_hit_batch(t.ctypes.data, len(t), dt, ns, w, variant,
+                                            k1.ctypes.data, x.ctypes.data, valid.ctypes.data)
+        assert code == 0
+        ok1, ox, ov = oracle.hit_batch(t, dt, ns, w)
+        np.testing.assert_array_equal(valid.astype(bool), ov)
+        np.testing.assert_array_equal(k1[ov], ok1[ov])
+        if variant == 0:
+            np.testing.assert_array_equal(bits(x[ov]), bits(ox[ov]))
+        else:
+            assert np.max(np.abs(x[ov] - ox[ov])) <= 2 ** -23
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+def test_run_cmp_matches_reference_pipeline(engine, cmp_small):
+    """velan::run_cmp (v-linear ScanConfig grid) vs the GPU with the same grid."""
+    _, ds = cmp_small
+    sub = ds.subset(range(8))
+    code, msg, ref = oracle.ref_run_pipeline(sub, "cmp", 1400.0, 4000.0, 41, 11, workers=4)
+    assert code == 0, msg
+    cfg = ScanConfig(vmin=1400.0, vmax=4000.0, nc=41, w=11)
+    r = engine.run_cmp(sub, cfg, emit_matrix=True)
+    np.testing.assert_array_equal(bits(r.values), bits(ref.matrix))
+    np.testing.assert_array_equal(r.best_idx, ref.best_idx)
+    np.testing.assert_array_equal(bits(r.stack_trace), bits(ref.best_stack))
+    assert r.stats.naive_fetches == ref.valid
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built")
+def test_run_crs_matches_reference_pipeline(engine):
+    w = configs.crs_small()
+    ds = w.spec.generate(count=24)
+    code, msg, ref = oracle.ref_run_pipeline(ds, "crs", 1500.0, 3500.0, 15, 11,
+                                             grid=(2, 1), apm=125.0, workers=4)
+    assert code == 0, msg
+    cfg = ScanConfig(vmin=1500.0, vmax=3500.0, nc=15, w=11)
+    r = engine.run_crs(ds, cfg, 125.0, emit_matrix=True)
+    np.testing.assert_array_equal(bits(r.values), bits(ref.matrix))
+    np.testing.assert_array_equal(r.best_idx, ref.best_idx)
+    np.testing.assert_array_equal(bits(r.stack_trace), bits(ref.best_stack))
+    assert r.stats.naive_fetches == ref.valid
