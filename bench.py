@@ -258,7 +258,6 @@ def main():
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         res = plan.execute(bi, bs, bst, stream=stream)
-    valid, nominal = int(res.valid_intersections), int(res.nominal_intersections)
 
     def barrier():
         if pg is not None:
@@ -280,6 +279,7 @@ def main():
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     launches = plan.launches() * args.steps
+    valid, nominal = int(res.valid_intersections), int(res.nominal_intersections)
 
     evals_rank = nominal * w * args.steps
     t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")

@@ -102,6 +102,12 @@ typedef struct velan_gpu_scan {
   const float* v; /* host [n_c]  velocity, m/s   (all operators)          */
   double apm;     /* CRS: closed-ball radius in m (neighbors_of,
                      crs_pipeline.hpp:162-180); ignored for NMO           */
+  /* Output rows [row_first, row_first + row_count) of the row order below
+   * (row_count 0 = all).  A shard of a longer line passes its own gathers
+   * plus the +-aperture halo and restricts the outputs to its block: the
+   * halo gathers then only feed neighbourhoods (run_crs's strips,
+   * crs_pipeline.hpp:341-347, as a replicated 1-D halo). */
+  int32_t row_first, row_count;
 } velan_gpu_scan;
 
 typedef struct velan_gpu_result {
@@ -109,12 +115,12 @@ typedef struct velan_gpu_result {
    * input order (run_cmp); CRS rows follow cdp_id order, ties by input index
    * (run_crs, crs_pipeline.hpp:449-459). */
   int32_t out_mem;        /* velan_mem of the four arrays               */
-  int32_t* best_idx;      /* [n_gathers][ns] flat candidate index       */
-  float* best_semblance;  /* [n_gathers][ns]  BestPick::semblance       */
-  float* best_stack;      /* [n_gathers][ns]  SemblanceMatrix::stack_trace */
-  float* matrix;          /* optional [n_gathers][ns][n_cand] (values),
+  int32_t* best_idx;      /* [rows][ns] flat candidate index            */
+  float* best_semblance;  /* [rows][ns]  BestPick::semblance            */
+  float* best_stack;      /* [rows][ns]  SemblanceMatrix::stack_trace   */
+  float* matrix;          /* optional [rows][ns][n_cand] (values),
                              NULL = not emitted                         */
-  int32_t* row_gather;    /* optional [n_gathers]: input index per row  */
+  int32_t* row_gather;    /* optional [rows]: input gather index per row */
   /* Filled by the call. */
   uint64_t valid_intersections;   /* CacheStats::naive_fetches          */
   uint64_t nominal_intersections; /* rows * ns * n_cand * traces/sweep  */
@@ -128,6 +134,9 @@ typedef struct velan_gpu_plan velan_gpu_plan;
 /* ABI version and the message of the last failure on this thread. */
 int velan_gpu_abi_version(void);
 const char* velan_gpu_last_error(void);
+/* Struct layout check for foreign bindings: writes sizeof and the offset of
+ * the last member of velan_gpu_dataset, _scan, _result, _synth (8 values). */
+int velan_gpu_abi_layout(int32_t* out8);
 /* Number of visible sm_100 devices (0 on a host without GPU). */
 int velan_gpu_device_count(void);
 
@@ -142,6 +151,17 @@ void velan_gpu_destroy(velan_gpu_ctx* ctx);
 /* Validate a scan without touching a device; mirrors ScanConfig::validate
  * (scan.hpp:61-78) and scan_sweep's ns > w + 1 check (scan.hpp:113-114). */
 int velan_gpu_validate(const velan_gpu_dataset* ds, const velan_gpu_scan* sc);
+
+/* Host-side sweep description, no device needed: the output row order
+ * (row_gather[rows]), traces per sweep (sweep_traces[rows]), the legs of
+ * every sweep in TraceSweep order (kernel.hpp:61-113) as CSR (leg_off[rows+1],
+ * leg_gather[n_legs], filled when leg_capacity >= n_legs) and the nominal
+ * intersection count.  Any output pointer may be NULL. */
+int velan_gpu_describe(const velan_gpu_dataset* ds, const velan_gpu_scan* sc,
+                       int32_t* row_gather, int32_t* sweep_traces,
+                       int32_t* leg_off, int32_t* leg_gather,
+                       int64_t leg_capacity, int64_t* n_legs,
+                       uint64_t* nominal);
 
 /* One-shot scans over host buffers (host->device, kernels, device->host).
  *  velan_gpu_cmp  replaces run_cmp   (cmp_pipeline.hpp:94-106); op NMO.

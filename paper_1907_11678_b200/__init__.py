@@ -17,6 +17,7 @@ from .api import (  # noqa: F401
     ScanConfig,
     ScanResult,
     VelanError,
+    describe,
     device_count,
     neighbors_of,
     run_cmp,
@@ -31,7 +32,7 @@ from . import configs  # noqa: F401
 __all__ = [
     "CacheStats", "ConfigError", "CrsAbcGrid", "Dataset", "DeviceError",
     "Engine", "ParameterError", "Plan", "ScanConfig", "ScanResult",
-    "VelanError", "device_count", "neighbors_of", "run_cmp", "run_crs",
+    "VelanError", "describe", "device_count", "neighbors_of", "run_cmp", "run_crs",
     "scan_cdp", "scan_central_cdp", "slowness_grid", "velocity_grid",
     "configs",
 ]

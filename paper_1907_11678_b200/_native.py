@@ -46,6 +46,8 @@ class Scan(C.Structure):
         ("b", C.c_void_p),
         ("v", C.c_void_p),
         ("apm", C.c_double),
+        ("row_first", C.c_int32),
+        ("row_count", C.c_int32),
     ]
 
 
@@ -91,8 +93,8 @@ class Synth(C.Structure):
         ("b_max", C.c_double),
         ("seed", C.c_uint64),
         ("gather_first", C.c_int32),
-        ("n_threads", C.c_int32),
         ("n_line", C.c_int32),
+        ("n_threads", C.c_int32),
     ]
 
 
@@ -100,11 +102,14 @@ class Synth(C.Structure):
 _P = C.c_void_p
 SIGNATURES = {
     "velan_gpu_abi_version": (C.c_int, []),
+    "velan_gpu_abi_layout": (C.c_int, [_P]),
     "velan_gpu_last_error": (C.c_char_p, []),
     "velan_gpu_device_count": (C.c_int, []),
     "velan_gpu_create": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_void_p)]),
     "velan_gpu_destroy": (None, [_P]),
     "velan_gpu_validate": (C.c_int, [C.POINTER(Dataset), C.POINTER(Scan)]),
+    "velan_gpu_describe": (C.c_int, [C.POINTER(Dataset), C.POINTER(Scan), _P, _P, _P, _P,
+                                     C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_uint64)]),
     "velan_gpu_cmp": (C.c_int, [_P, C.POINTER(Dataset), C.POINTER(Scan), C.POINTER(Result)]),
     "velan_gpu_crs": (C.c_int, [_P, C.POINTER(Dataset), C.POINTER(Scan), C.POINTER(Result)]),
     "velan_gpu_plan_create": (C.c_int, [_P, C.POINTER(Dataset), C.POINTER(Scan), C.POINTER(C.c_void_p)]),

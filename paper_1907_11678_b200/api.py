@@ -289,8 +289,11 @@ def _dataset_struct(ds: Dataset) -> N.Dataset:
 
 
 def _scan_struct(op: int, variant: str, w: int, v: np.ndarray,
-                 abc: Optional[CrsAbcGrid], apm: float, keep: list) -> N.Scan:
+                 abc: Optional[CrsAbcGrid], apm: float, keep: list,
+                 rows: Optional[tuple] = None) -> N.Scan:
     sc = N.Scan()
+    if rows is not None:
+        sc.row_first, sc.row_count = int(rows[0]), int(rows[1])
     sc.op = op
     if variant not in VARIANTS:
         raise ConfigError(f"ScanConfig: unknown kernel variant {variant!r}")
@@ -337,12 +340,12 @@ class Engine:
 
     def _run(self, fn, ds: Dataset, op: int, variant: str, w: int,
              v: np.ndarray, abc: Optional[CrsAbcGrid], apm: float,
-             emit_matrix: bool, out=None) -> ScanResult:
+             emit_matrix: bool, out=None, rows=None) -> ScanResult:
         lib = N.load()
         keep: list = []
-        sc = _scan_struct(op, variant, w, v, abc, apm, keep)
+        sc = _scan_struct(op, variant, w, v, abc, apm, keep, rows)
         dss = _dataset_struct(ds)
-        G = ds.ncdps
+        G = ds.ncdps if rows is None else int(rows[1])
         ns = dss.ns
         ncand = abc.ncand if abc is not None else len(v)
         if out is not None:  # caller-provided host buffers (e.g. pinned)
@@ -374,23 +377,28 @@ class Engine:
                           float(res.kernel_ms), float(res.total_ms))
 
     def run_cmp(self, ds: Dataset, config: ScanConfig,
-                emit_matrix: bool = False, out=None) -> ScanResult:
+                emit_matrix: bool = False, out=None, rows=None) -> ScanResult:
+        """``rows`` = (first, count) restricts the outputs to a row block."""
         config.validate()
         return self._run(N.load().velan_gpu_cmp, ds, N.OP_NMO,
                          config.kernel_variant, config.w, config.grid(), None,
-                         0.0, emit_matrix, out)
+                         0.0, emit_matrix, out, rows)
 
     def run_crs(self, ds: Dataset, config: ScanConfig, apm: float,
                 abc: Optional[CrsAbcGrid] = None,
-                emit_matrix: bool = False, out=None) -> ScanResult:
+                emit_matrix: bool = False, out=None, rows=None) -> ScanResult:
+        """``rows`` = (first, count): a shard's own block of the cdp_id-ordered
+        rows; the remaining gathers are halo feeding the neighbourhoods."""
         config.validate()
         op = N.OP_CRS_ABC if abc is not None else N.OP_CRS_D2
         return self._run(N.load().velan_gpu_crs, ds, op, config.kernel_variant,
-                         config.w, config.grid(), abc, apm, emit_matrix, out)
+                         config.w, config.grid(), abc, apm, emit_matrix, out,
+                         rows)
 
     def plan(self, ds: Dataset, config: ScanConfig, op: str = "nmo",
-             apm: float = 0.0, abc: Optional[CrsAbcGrid] = None) -> "Plan":
-        return Plan(self, ds, config, op, apm, abc)
+             apm: float = 0.0, abc: Optional[CrsAbcGrid] = None,
+             rows: Optional[tuple] = None) -> "Plan":
+        return Plan(self, ds, config, op, apm, abc, rows)
 
 
 class Plan:
@@ -398,20 +406,21 @@ class Plan:
     once; execute() only launches the scan kernels."""
 
     def __init__(self, engine: Engine, ds: Dataset, config: ScanConfig,
-                 op: str, apm: float, abc: Optional[CrsAbcGrid]):
+                 op: str, apm: float, abc: Optional[CrsAbcGrid],
+                 rows: Optional[tuple] = None):
         lib = N.load()
         config.validate()
         opc = {"nmo": N.OP_NMO, "d2": N.OP_CRS_D2, "abc": N.OP_CRS_ABC}[op]
         self._keep: list = []
         sc = _scan_struct(opc, config.kernel_variant, config.w, config.grid(),
-                          abc, apm, self._keep)
+                          abc, apm, self._keep, rows)
         dss = _dataset_struct(ds)
         self._ds = ds  # keep device samples alive
         h = C.c_void_p()
         _raise(lib.velan_gpu_plan_create(engine._h, C.byref(dss), C.byref(sc),
                                          C.byref(h)), "velan_gpu_plan_create")
         self._h = h
-        self.rows = ds.ncdps
+        self.rows = ds.ncdps if rows is None else int(rows[1])
         self.ns = dss.ns
         self.ncand = abc.ncand if abc is not None else len(config.grid())
 
@@ -543,6 +552,42 @@ def scan_central_cdp(dataset: Dataset, central: int, neighbors: Sequence[int],
                       r.cdp_id[keep],
                       None if r.values is None else r.values[keep], r.stats,
                       r.kernel_ms, r.total_ms)
+
+
+@dataclass
+class SweepPlan:
+    """Host-side description of the TraceSweeps a scan will run."""
+    row_gather: np.ndarray    # input gather per output row
+    sweep_traces: np.ndarray  # traces per sweep
+    leg_off: np.ndarray       # CSR offsets [rows + 1]
+    leg_gather: np.ndarray    # gathers of every sweep, central first
+    nominal_intersections: int
+
+
+def describe(dataset: Dataset, config: ScanConfig, op: str = "nmo",
+             apm: float = 0.0, abc: Optional[CrsAbcGrid] = None,
+             rows: Optional[tuple] = None) -> SweepPlan:
+    """The sweeps (central gather + closed-ball neighbours in cdp_id order)
+    the library builds for a scan — host only, no device needed."""
+    lib = N.load()
+    opc = {"nmo": N.OP_NMO, "d2": N.OP_CRS_D2, "abc": N.OP_CRS_ABC}[op]
+    keep: list = []
+    sc = _scan_struct(opc, config.kernel_variant, config.w, config.grid(),
+                      abc, apm, keep, rows)
+    dss = _dataset_struct(dataset)
+    n_rows = dataset.ncdps if rows is None else int(rows[1])
+    rg = np.zeros(n_rows, np.int32)
+    st = np.zeros(n_rows, np.int32)
+    lo = np.zeros(n_rows + 1, np.int32)
+    nl, nom = C.c_int64(0), C.c_uint64(0)
+    _raise(lib.velan_gpu_describe(C.byref(dss), C.byref(sc), _ptr(rg), _ptr(st),
+                                  _ptr(lo), None, 0, C.byref(nl), C.byref(nom)),
+           "velan_gpu_describe")
+    lg = np.zeros(max(nl.value, 1), np.int32)
+    _raise(lib.velan_gpu_describe(C.byref(dss), C.byref(sc), None, None, None,
+                                  _ptr(lg), nl.value, C.byref(nl), C.byref(nom)),
+           "velan_gpu_describe")
+    return SweepPlan(rg, st, lo, lg[: nl.value], int(nom.value))
 
 
 def device_count() -> int:

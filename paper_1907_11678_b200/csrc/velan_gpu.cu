@@ -23,6 +23,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstddef>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -158,6 +159,10 @@ void validate(const velan_gpu_dataset* ds, const velan_gpu_scan* sc,
   }
   // dataset shape
   if (ds->n_gathers < 0) throw ApiError(VELAN_GPU_EPARAM, "n_gathers < 0");
+  if (sc->row_first < 0 || sc->row_count < 0 ||
+      static_cast<long long>(sc->row_first) + sc->row_count > ds->n_gathers ||
+      (sc->row_count == 0 && sc->row_first != 0))
+    throw ApiError(VELAN_GPU_EPARAM, "output row range outside the dataset");
   if (ds->n_gathers == 0) return;  // run_cmp / run_crs return {} (no error)
   if (crs && !(sc->apm > 0.0))
     throw ApiError(VELAN_GPU_ECONFIG, "partition: apm must be > 0");
@@ -257,6 +262,12 @@ HostSweep build_sweep(const velan_gpu_dataset* ds, const velan_gpu_scan* sc) {
   if (sc->op != VELAN_OP_NMO)
     std::stable_sort(h.row_gather.begin(), h.row_gather.end(),
                      [&](int x, int y) { return ds->cdp_id[x] < ds->cdp_id[y]; });
+  if (sc->row_count > 0) {  // a shard's own block; the rest is halo
+    h.row_gather.erase(h.row_gather.begin(),
+                       h.row_gather.begin() + sc->row_first);
+    h.row_gather.resize(sc->row_count);
+    h.rows = sc->row_count;
+  }
   h.leg_off.assign(1, 0);
   h.row_traces.resize(h.rows);
   if (sc->op == VELAN_OP_NMO) {
@@ -702,6 +713,19 @@ int velan_gpu_abi_version(void) { return VELAN_GPU_ABI_VERSION; }
 
 const char* velan_gpu_last_error(void) { return g_last_error.c_str(); }
 
+int velan_gpu_abi_layout(int32_t* out8) {
+  if (!out8) return VELAN_GPU_EPARAM;
+  out8[0] = sizeof(velan_gpu_dataset);
+  out8[1] = offsetof(velan_gpu_dataset, samples_device);
+  out8[2] = sizeof(velan_gpu_scan);
+  out8[3] = offsetof(velan_gpu_scan, row_count);
+  out8[4] = sizeof(velan_gpu_result);
+  out8[5] = offsetof(velan_gpu_result, total_ms);
+  out8[6] = sizeof(velan_gpu_synth);
+  out8[7] = offsetof(velan_gpu_synth, n_threads);
+  return VELAN_GPU_OK;
+}
+
 int velan_gpu_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) {
@@ -758,6 +782,37 @@ void velan_gpu_destroy(velan_gpu_ctx* ctx) {
 int velan_gpu_validate(const velan_gpu_dataset* ds, const velan_gpu_scan* sc) {
   VG_API_BEGIN
   validate(ds, sc, sc && sc->op != VELAN_OP_NMO);
+  return VELAN_GPU_OK;
+  VG_API_END
+}
+
+int velan_gpu_describe(const velan_gpu_dataset* ds, const velan_gpu_scan* sc,
+                       int32_t* row_gather, int32_t* sweep_traces,
+                       int32_t* leg_off, int32_t* leg_gather,
+                       int64_t leg_capacity, int64_t* n_legs,
+                       uint64_t* nominal) {
+  VG_API_BEGIN
+  validate(ds, sc, sc && sc->op != VELAN_OP_NMO);
+  if (ds->n_gathers == 0) {
+    if (n_legs) *n_legs = 0;
+    if (nominal) *nominal = 0;
+    if (leg_off) leg_off[0] = 0;
+    return VELAN_GPU_OK;
+  }
+  const HostSweep h = build_sweep(ds, sc);
+  uint64_t nom = 0;
+  for (int r = 0; r < h.rows; ++r) {
+    if (row_gather) row_gather[r] = h.row_gather[r];
+    if (sweep_traces) sweep_traces[r] = static_cast<int32_t>(h.row_traces[r]);
+    nom += static_cast<uint64_t>(h.row_traces[r]) * h.ns * h.ncand;
+  }
+  const int64_t nl = static_cast<int64_t>(h.leg_gather.size());
+  if (n_legs) *n_legs = nl;
+  if (nominal) *nominal = nom;
+  if (leg_off)
+    for (int r = 0; r <= h.rows; ++r) leg_off[r] = h.leg_off[r];
+  if (leg_gather && leg_capacity >= nl)
+    for (int64_t i = 0; i < nl; ++i) leg_gather[i] = h.leg_gather[i];
   return VELAN_GPU_OK;
   VG_API_END
 }
