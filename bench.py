@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--variant", default="fast", choices=["fast", "exact"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="target CPU time of the cpu_baseline sample")
+    ap.add_argument("--gathers", type=int, default=0,
+                    help="override midpoints per GPU (profiling slices only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -239,6 +241,9 @@ def main():
     from paper_1907_11678_b200 import Dataset, Engine, _native, configs
     wl = configs.WORKLOADS[args.workload]()
     wl.config.kernel_variant = args.variant
+    if args.gathers > 0:
+        from dataclasses import replace
+        wl.spec = replace(wl.spec, n_gathers=args.gathers)
     G = wl.spec.n_gathers
     # weak scaling: rank r scans gathers [r*G, (r+1)*G) of a world*G line
     t_gen = time.perf_counter()

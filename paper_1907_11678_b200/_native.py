@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libvelan_gpu.so")
+LIB_PATH = os.environ.get("VELAN_GPU_LIB") or os.path.join(_HERE, "_lib", "libvelan_gpu.so")
 
 OK, ECONFIG, EPARAM, ERUNTIME, ENODEV = 0, 1, 2, 3, 4
 OP_NMO, OP_CRS_D2, OP_CRS_ABC = 0, 1, 2

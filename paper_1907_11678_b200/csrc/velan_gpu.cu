@@ -76,7 +76,8 @@ struct KernelChoice {
 
 template <int OPK, int VAR, int WMAX, bool FIXED>
 KernelChoice pick() {
-  constexpr int CC = WMAX > 16 ? 2 : 4;
+  // FAST keeps two accumulator rows (P, R) per pair: half the pairs
+  constexpr int CC = VAR == VAR_FAST ? (WMAX > 16 ? 1 : 2) : (WMAX > 16 ? 2 : 4);
   return KernelChoice{&semblance_scan_kernel<OPK, VAR, WMAX, FIXED, CC>, CC};
 }
 
@@ -177,9 +178,11 @@ void validate(const velan_gpu_dataset* ds, const velan_gpu_scan* sc,
   if (ds->ns <= sc->w + 1)
     throw ApiError(VELAN_GPU_ECONFIG,
                    "scan_sweep: window does not fit trace length");
-  if (ds->ns > 24000)
+  // one trace must fit a staging stage (kStages stages per CTA)
+  if (ds->ns > (sc->variant == VELAN_VARIANT_FAST ? 6000 : 18000))
     throw ApiError(VELAN_GPU_ECONFIG,
-                   "ns > 24000 exceeds the shared-memory staging capacity");
+                   "ns exceeds the shared-memory staging capacity of the "
+                   "kernel variant (FAST 6000, EXACT 18000 samples)");
   for (int g = 0; g < ds->n_gathers; ++g) {
     if (ds->ntraces[g] < 0 || ds->ntraces[g] > ds->max_traces)
       throw ApiError(VELAN_GPU_EPARAM,
@@ -356,7 +359,7 @@ struct DevBuf {
 };
 
 enum BufId {
-  B_SAMPLES, B_H2, B_NTR, B_LEGOFF, B_LEGG, B_LEGD2, B_LEGDM, B_T0, B_A, B_B,
+  B_SAMPLES, B_EC, B_H2, B_NTR, B_LEGOFF, B_LEGG, B_LEGD2, B_LEGDM, B_T0, B_A, B_B,
   B_V, B_BIDX, B_BS, B_BST, B_MAT, B_VALID, B_COUNT
 };
 
@@ -485,8 +488,13 @@ void set_smem_attr(KernelFn fn, size_t smem) {
                                static_cast<int>(smem)));
 }
 
-int staging_cap(int ns) {
-  int cap = std::max(4096, ((ns + 3) / 4) * 4 + 8);
+// Floats per staging stage: two 256-thread CTAs per SM fit with kStages
+// stages (FAST stages also hold the float2 window energies).
+#ifndef VELAN_FAST_CAP
+#define VELAN_FAST_CAP 2560
+#endif
+int staging_cap(int ns, bool fast) {
+  int cap = std::max(fast ? VELAN_FAST_CAP : 4096, ((ns + 3) / 4) * 4 + 8);
   return (cap + 31) / 32 * 32;
 }
 
@@ -580,7 +588,12 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
   p.w = h.w;
   p.vec4 = (h.ns % 4 == 0) &&
            (reinterpret_cast<uintptr_t>(d_samples) % 16 == 0);
-  p.cap = staging_cap(h.ns);
+  const bool fast = sc->variant == VELAN_VARIANT_FAST;
+  p.cap = staging_cap(h.ns, fast);
+  if (fast) {
+    D.bufs[B_EC].ensure(std::max<size_t>(1, static_cast<size_t>(L) * trace_floats * 8 + 64));
+    p.ec = D.bufs[B_EC].as<float2>();
+  }
   p.dt = h.dt;
   {
     const double inv = 1.0 / h.dt;
@@ -593,11 +606,28 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
   p.best_stack = d_bst;
   p.matrix = d_mat;
   p.valid = D.bufs[B_VALID].as<unsigned long long>();
-  const size_t smem = static_cast<size_t>(2) * p.cap * sizeof(float);
+  // per-row metadata staged in shared memory by the kernel
+  int max_legs = 1, max_sweep = 1;
+  for (int r = 0; r < rows; ++r) {
+    max_legs = std::max(max_legs, s.leg_off[r + 1] - s.leg_off[r]);
+    max_sweep = std::max<long long>(max_sweep, h.row_traces[s.r0 + r]);
+  }
+  p.max_legs = max_legs;
+  p.max_sweep = max_sweep;
+  const size_t meta_floats = 5 * static_cast<size_t>(max_legs) + max_sweep +
+                             h.n_a + h.n_b + h.n_c;
+  const size_t smem =
+      (static_cast<size_t>(kStages) * p.cap * (fast ? 3 : 1) + meta_floats) *
+      sizeof(float);
+  if (smem > 227 * 1024)
+    throw ApiError(VELAN_GPU_ECONFIG,
+                   "scan exceeds the 227 KB shared-memory budget of a CTA "
+                   "(too many traces per sweep or candidates)");
   set_smem_attr(kc.fn, smem);
 
   const int nwaves = static_cast<int>(s.wave_need.size());
   int uploaded = 0;
+  int ec_done = 0;
   for (int wv = 0; wv < nwaves; ++wv) {
     if (upload_samples && s.wave_need[wv] > uploaded) {
       // contiguous runs of global gathers -> one copy each
@@ -616,6 +646,17 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
       uploaded = need;
       VG_CUDA(cudaEventRecord(D.ev(2 * nwaves + wv), D.copy_stream));
       VG_CUDA(cudaStreamWaitEvent(st, D.ev(2 * nwaves + wv), 0));
+    }
+    if (fast && s.wave_need[wv] > ec_done) {
+      // window-energy tables of the gathers this wave adds (part of the scan)
+      const long long ntr = static_cast<long long>(s.wave_need[wv] - ec_done) * h.M;
+      const size_t off = static_cast<size_t>(ec_done) * trace_floats;
+      dim3 eg(static_cast<unsigned>(ntr), (h.ns + 255) / 256);
+      window_energy_kernel<<<eg, 256, (256 + h.w + 1) * sizeof(float), st>>>(
+          d_samples + off, D.bufs[B_EC].as<float2>() + off, ntr, h.ns, h.w);
+      VG_CUDA(cudaGetLastError());
+      ec_done = s.wave_need[wv];
+      ++out.launches;
     }
     const int rb = s.wave_rows[wv], re = s.wave_rows[wv + 1];
     p.row_first = rb;
