@@ -179,10 +179,10 @@ void validate(const velan_gpu_dataset* ds, const velan_gpu_scan* sc,
     throw ApiError(VELAN_GPU_ECONFIG,
                    "scan_sweep: window does not fit trace length");
   // one trace must fit a staging stage (kStages stages per CTA)
-  if (ds->ns > (sc->variant == VELAN_VARIANT_FAST ? 6000 : 18000))
+  if (ds->ns > (sc->variant == VELAN_VARIANT_FAST ? 6800 : 27000))
     throw ApiError(VELAN_GPU_ECONFIG,
                    "ns exceeds the shared-memory staging capacity of the "
-                   "kernel variant (FAST 6000, EXACT 18000 samples)");
+                   "kernel variant (FAST 6800, EXACT 27000 samples)");
   for (int g = 0; g < ds->n_gathers; ++g) {
     if (ds->ntraces[g] < 0 || ds->ntraces[g] > ds->max_traces)
       throw ApiError(VELAN_GPU_EPARAM,
@@ -490,8 +490,9 @@ void set_smem_attr(KernelFn fn, size_t smem) {
 
 // Floats per staging stage: two 256-thread CTAs per SM fit with kStages
 // stages (FAST stages also hold the float2 window energies).
+// FAST stages hold float4 entries (16 B), EXACT stages fp32 samples.
 #ifndef VELAN_FAST_CAP
-#define VELAN_FAST_CAP 2560
+#define VELAN_FAST_CAP 2880
 #endif
 int staging_cap(int ns, bool fast) {
   int cap = std::max(fast ? VELAN_FAST_CAP : 4096, ((ns + 3) / 4) * 4 + 8);
@@ -586,13 +587,19 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
   p.Mmax = h.M;
   p.ns = h.ns;
   p.w = h.w;
-  p.vec4 = (h.ns % 4 == 0) &&
-           (reinterpret_cast<uintptr_t>(d_samples) % 16 == 0);
+  // TMA bulk copies need 16-byte aligned trace segments: EXACT stages the
+  // samples (ns % 4), FAST its own pair/energy tables (ns % 2)
+  p.vec4 = sc->variant == VELAN_VARIANT_FAST
+               ? (h.ns % 2 == 0)
+               : (h.ns % 4 == 0) &&
+                     (reinterpret_cast<uintptr_t>(d_samples) % 16 == 0);
   const bool fast = sc->variant == VELAN_VARIANT_FAST;
   p.cap = staging_cap(h.ns, fast);
   if (fast) {
-    D.bufs[B_EC].ensure(std::max<size_t>(1, static_cast<size_t>(L) * trace_floats * 8 + 64));
-    p.ec = D.bufs[B_EC].as<float2>();
+    // pairs then energies, 8 B per sample each
+    D.bufs[B_EC].ensure(std::max<size_t>(1, static_cast<size_t>(L) * trace_floats * 16 + 64));
+    p.pairs = D.bufs[B_EC].as<float2>();
+    p.ec = p.pairs + static_cast<size_t>(L) * trace_floats;
   }
   p.dt = h.dt;
   {
@@ -617,7 +624,7 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
   const size_t meta_floats = 5 * static_cast<size_t>(max_legs) + max_sweep +
                              h.n_a + h.n_b + h.n_c;
   const size_t smem =
-      (static_cast<size_t>(kStages) * p.cap * (fast ? 3 : 1) + meta_floats) *
+      (static_cast<size_t>(kStages) * p.cap * (fast ? 4 : 1) + meta_floats) *
       sizeof(float);
   if (smem > 227 * 1024)
     throw ApiError(VELAN_GPU_ECONFIG,
@@ -652,8 +659,9 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
       const long long ntr = static_cast<long long>(s.wave_need[wv] - ec_done) * h.M;
       const size_t off = static_cast<size_t>(ec_done) * trace_floats;
       dim3 eg(static_cast<unsigned>(ntr), (h.ns + 255) / 256);
-      window_energy_kernel<<<eg, 256, (256 + h.w + 1) * sizeof(float), st>>>(
-          d_samples + off, D.bufs[B_EC].as<float2>() + off, ntr, h.ns, h.w);
+      pair_energy_kernel<<<eg, 256, (256 + h.w + 1) * sizeof(float), st>>>(
+          d_samples + off, const_cast<float2*>(p.pairs) + off,
+          const_cast<float2*>(p.ec) + off, ntr, h.ns, h.w);
       VG_CUDA(cudaGetLastError());
       ec_done = s.wave_need[wv];
       ++out.launches;

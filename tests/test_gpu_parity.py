@@ -34,11 +34,21 @@ def assert_bitwise(gpu, ref_cells, ns, ncand=None):
     assert gpu.stats.naive_fetches == ref_cells.valid
 
 
-def assert_close(gpu, ref_cells, ns, ncand, stack_floor):
+def assert_close(gpu, ref_cells, ns, ncand, stack_floor, sem_floor=0.0):
+    """FAST variant check.  sem_floor = 0: pure relative 1e-4 (the north-star
+    bound, used on BASELINE-like data).  sem_floor > 0: relative 1e-4 plus an
+    absolute floor on the semblance scale [0, M] for adversarial random data,
+    where sum_j num_j cancels and any reassociation — the reference's own
+    blocked vs oracle included — differs at ~eps*M (the reference's tests use
+    the same kind of margin for its vectorized variant, test_kernel.cpp:221-226)."""
     G = gpu.best_idx.shape[0]
     m_gpu = gpu.values.reshape(G * ns, ncand)
     rep = oracle.compare(m_gpu, ref_cells.matrix)
-    assert rep["max_rel_err"] <= SEM_RTOL, rep
+    if sem_floor == 0.0:
+        assert rep["max_rel_err"] <= SEM_RTOL, rep
+    else:
+        d = np.abs(m_gpu.astype(np.float64) - ref_cells.matrix)
+        assert np.all(d <= SEM_RTOL * np.abs(ref_cells.matrix) + sem_floor), float(d.max())
     assert rep["argmax_mismatches"] == 0, rep
     same = gpu.best_idx.reshape(-1) == ref_cells.best_idx
     # stack at the pick: relative with an absolute floor (near-cancelling mean)
@@ -100,22 +110,30 @@ def test_crs_abc_subset(engine, variant):
 
 
 @pytest.mark.parametrize("w", [1, 2, 3, 4, 5, 8, 11, 13, 15, 16, 21, 32])
-def test_window_lengths_exact(engine, w):
+@pytest.mark.parametrize("ns,variant", [(131, "exact"), (132, "exact"),
+                                        (131, "fast"), (132, "fast")])
+def test_window_lengths(engine, w, ns, variant):
+    """Every window length, through both staging paths (ns % 4 / ns % 2
+    decide between TMA bulk copies and the synchronous fallback)."""
     rng = np.random.default_rng(100 + w)
-    G, M, ns = 3, 7, 131  # ns % 4 != 0: synchronous staging path
+    G, M = 3, 7
     samples = rng.uniform(-1, 1, (G, M, ns)).astype(np.float32)
     coords = np.zeros((G, M, 4), np.float32)
     coords[:, :, 2] = np.linspace(0, 40, M)[None, :]
     from paper_1907_11678_b200 import Dataset
     ds = Dataset(samples, coords, np.full(G, M, np.int32), np.arange(G, dtype=np.uint32), 244)
     v = velocity_grid(2000.0, 3000.0, 9)
-    cfg = ScanConfig(w=w, velocities=v)
+    cfg = ScanConfig(w=w, velocities=v, kernel_variant=variant)
     if ns <= w + 1:
         pytest.skip("window does not fit")
     r = engine.run_cmp(ds, cfg, emit_matrix=True)
     rows, ks = oracle.all_cells(G, ns)
     ref = oracle.run_cells(ds, "nmo", w, v, rows, ks, matrix=True)
-    assert_bitwise(r, ref, ns, len(v))
+    if variant == "exact":
+        assert_bitwise(r, ref, ns, len(v))
+    else:
+        # U[-1, 1] noise, M = 7: semblance scale M, floor 2e-6 * M
+        assert_close(r, ref, ns, len(v), 1e-6, sem_floor=2e-6 * M)
 
 
 def test_hit_exact_matches_reference_rule():
