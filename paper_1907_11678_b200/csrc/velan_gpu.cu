@@ -77,7 +77,8 @@ struct KernelChoice {
 template <int OPK, int VAR, int WMAX, bool FIXED>
 KernelChoice pick() {
   // FAST keeps two accumulator rows (P, R) per pair: half the pairs
-  constexpr int CC = VAR == VAR_FAST ? (WMAX > 16 ? 1 : 2) : (WMAX > 16 ? 2 : 4);
+  // candidates per warp (the group of a CTA is kWarps x CC candidates)
+  constexpr int CC = WMAX > 16 ? 1 : 2;
   return KernelChoice{&semblance_scan_kernel<OPK, VAR, WMAX, FIXED, CC>, CC};
 }
 
@@ -448,7 +449,7 @@ Shard make_shard(const HostSweep& h, const velan_gpu_dataset* ds, int r0,
   for (int r = r0; r < r1; ++r)
     s.nominal += h.row_traces[r] * static_cast<long long>(h.ns) * h.ncand;
   // waves: ~equal nominal work, >= 2 waves of CTAs per launch when possible
-  const long long per_row_ctas = (h.ns + kThreads - 1) / kThreads;
+  const long long per_row_ctas = (h.ns + kT0 - 1) / kT0;
   const long long rows = r1 - r0;
   long long total_work = 0;
   for (int r = r0; r < r1; ++r) total_work += h.row_traces[r];
@@ -492,10 +493,10 @@ void set_smem_attr(KernelFn fn, size_t smem) {
 // stages (FAST stages also hold the float2 window energies).
 // FAST stages hold float4 entries (16 B), EXACT stages fp32 samples.
 #ifndef VELAN_FAST_CAP
-#define VELAN_FAST_CAP 2880
+#define VELAN_FAST_CAP 2560
 #endif
 int staging_cap(int ns, bool fast) {
-  int cap = std::max(fast ? VELAN_FAST_CAP : 4096, ((ns + 3) / 4) * 4 + 8);
+  int cap = std::max(fast ? VELAN_FAST_CAP : 8192, ((ns + 3) / 4) * 4 + 8 + (fast ? 40 : 0));
   return (cap + 31) / 32 * 32;
 }
 
@@ -668,7 +669,7 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
     }
     const int rb = s.wave_rows[wv], re = s.wave_rows[wv + 1];
     p.row_first = rb;
-    dim3 grid((h.ns + kThreads - 1) / kThreads, re - rb);
+    dim3 grid((h.ns + kT0 - 1) / kT0, re - rb);
     VG_CUDA(cudaEventRecord(D.ev(2 * wv), st));
     kc.fn<<<grid, kThreads, smem, st>>>(p);
     VG_CUDA(cudaGetLastError());
