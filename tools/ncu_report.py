@@ -66,11 +66,13 @@ def main():
               ", ".join(f"{k} {100 * v / tot:.1f}%" for k, v in sorted(st.items(), key=lambda x: -x[1])[:10]))
     src = source(rep)
     if src:
-        top = max(int(s.get("Instructions Executed") or 0) for s in src)
+        # the hot loop = the most executed FFMA (spin-wait loops excluded)
+        top = max(int(s.get("Instructions Executed") or 0) for s in src
+                  if "FFMA" in s.get("Source", ""))
         cnt = Counter()
         for s in src:
             n = int(s.get("Instructions Executed") or 0)
-            if n >= 0.7 * top:
+            if 0.7 * top <= n <= 1.3 * top:
                 t = s["Source"].strip()
                 op = (t.split()[1] if t.startswith("@") else t.split()[0]).split(".")[0]
                 cnt[op] += n
