@@ -1,0 +1,16 @@
+#!/bin/bash
+# One GPU call: the default bench, other workloads, the reference arm, and the
+# ncu launch list + DRAM traffic of the default bench command.
+set -x
+mkdir -p gpurun_out/rb
+python bench.py > gpurun_out/rb/bench_default.json 2> gpurun_out/rb/bench_default.err
+python bench.py --workload cmp_small --cpu-seconds 5 > gpurun_out/rb/bench_cmp_small.json 2> gpurun_out/rb/bench_cmp_small.err
+python bench.py --workload crs_small --steps 2 --warmup 1 --cpu-seconds 10 > gpurun_out/rb/bench_crs_small.json 2> gpurun_out/rb/bench_crs_small.err
+python bench.py --workload crs_large --gathers 64 --steps 1 --warmup 1 --no-e2e --cpu-seconds 10 > gpurun_out/rb/bench_crs_large64.json 2> gpurun_out/rb/bench_crs_large64.err
+python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/rb/bench_reference.json 2> gpurun_out/rb/bench_reference.err
+python bench.py --variant exact --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/rb/bench_exact.json 2> gpurun_out/rb/bench_exact.err
+# ncu: launch list (every launch, device time) and DRAM bytes of the default command
+python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/rb/plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file gpurun_out/rb/launches.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/rb/ncu_launch.log 2>&1
+echo done
