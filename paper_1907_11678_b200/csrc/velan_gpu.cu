@@ -72,18 +72,34 @@ using KernelFn = void (*)(ScanParams);
 struct KernelChoice {
   KernelFn fn = nullptr;
   int cc = 0;
+  int cap = 0;  // compile-time stage capacity (FAST), 0 = runtime (EXACT)
 };
 
-template <int OPK, int VAR, int WMAX, bool FIXED>
+// FAST stage capacities (entries): the default, and the one for traces
+// longer than it holds (one CTA per SM)
+#ifndef VELAN_FAST_CAP
+#define VELAN_FAST_CAP 2560
+#endif
+constexpr int kFastCap = VELAN_FAST_CAP;
+constexpr int kFastCapBig = 6016;  // ns <= 5968
+
+template <int OPK, int VAR, int WMAX, bool FIXED, int CAPF = 0>
 KernelChoice pick() {
   // FAST keeps two accumulator rows (P, R) per pair: half the pairs
   // candidates per warp (the group of a CTA is kWarps x CC candidates)
   constexpr int CC = WMAX > 16 ? 1 : 2;
-  return KernelChoice{&semblance_scan_kernel<OPK, VAR, WMAX, FIXED, CC>, CC};
+  constexpr int CAP = VAR == VAR_FAST ? (CAPF ? CAPF : kFastCap) : 0;
+  return KernelChoice{&semblance_scan_kernel<OPK, VAR, WMAX, FIXED, CC, CAP>, CC, CAP};
 }
 
 template <int OPK, int VAR>
-KernelChoice pick_w(int w) {
+KernelChoice pick_w(int w, bool big) {
+  if (VAR == VAR_FAST && big) {  // rare: generic windows only
+    if (w <= 4) return pick<OPK, VAR, 4, false, kFastCapBig>();
+    if (w <= 8) return pick<OPK, VAR, 8, false, kFastCapBig>();
+    if (w <= 16) return pick<OPK, VAR, 16, false, kFastCapBig>();
+    return pick<OPK, VAR, 32, false, kFastCapBig>();
+  }
   switch (w) {
     case 1: return pick<OPK, VAR, 1, true>();
     case 2: return pick<OPK, VAR, 2, true>();
@@ -100,13 +116,13 @@ KernelChoice pick_w(int w) {
   return pick<OPK, VAR, 32, false>();
 }
 
-KernelChoice choose_kernel(int op, int variant, int w) {
+KernelChoice choose_kernel(int op, int variant, int w, bool big) {
   const int opk = op == VELAN_OP_CRS_ABC ? OPK_ABC : OPK_Q;
   if (opk == OPK_Q)
-    return variant == VELAN_VARIANT_EXACT ? pick_w<OPK_Q, VAR_EXACT>(w)
-                                          : pick_w<OPK_Q, VAR_FAST>(w);
-  return variant == VELAN_VARIANT_EXACT ? pick_w<OPK_ABC, VAR_EXACT>(w)
-                                        : pick_w<OPK_ABC, VAR_FAST>(w);
+    return variant == VELAN_VARIANT_EXACT ? pick_w<OPK_Q, VAR_EXACT>(w, big)
+                                          : pick_w<OPK_Q, VAR_FAST>(w, big);
+  return variant == VELAN_VARIANT_EXACT ? pick_w<OPK_ABC, VAR_EXACT>(w, big)
+                                        : pick_w<OPK_ABC, VAR_FAST>(w, big);
 }
 
 // ---------------------------------------------------------------------------
@@ -180,10 +196,10 @@ void validate(const velan_gpu_dataset* ds, const velan_gpu_scan* sc,
     throw ApiError(VELAN_GPU_ECONFIG,
                    "scan_sweep: window does not fit trace length");
   // one trace must fit a staging stage (kStages stages per CTA)
-  if (ds->ns > (sc->variant == VELAN_VARIANT_FAST ? 6800 : 27000))
+  if (ds->ns > (sc->variant == VELAN_VARIANT_FAST ? 5960 : 27000))
     throw ApiError(VELAN_GPU_ECONFIG,
                    "ns exceeds the shared-memory staging capacity of the "
-                   "kernel variant (FAST 6800, EXACT 27000 samples)");
+                   "kernel variant (FAST 5960, EXACT 27000 samples)");
   for (int g = 0; g < ds->n_gathers; ++g) {
     if (ds->ntraces[g] < 0 || ds->ntraces[g] > ds->max_traces)
       throw ApiError(VELAN_GPU_EPARAM,
@@ -489,14 +505,16 @@ void set_smem_attr(KernelFn fn, size_t smem) {
                                static_cast<int>(smem)));
 }
 
-// Floats per staging stage: two 256-thread CTAs per SM fit with kStages
-// stages (FAST stages also hold the float2 window energies).
-// FAST stages hold float4 entries (16 B), EXACT stages fp32 samples.
-#ifndef VELAN_FAST_CAP
-#define VELAN_FAST_CAP 2560
-#endif
+// Entries per staging stage: two 256-thread CTAs per SM fit with kStages
+// stages.  FAST entries are 16 B (a sample pair and its window energies),
+// EXACT entries fp32 samples.  A stage must hold one whole trace plus the
+// zero pad.
+int staging_need(int ns, bool fast) {
+  return ((ns + 3) / 4) * 4 + 8 + (fast ? 40 : 0);
+}
 int staging_cap(int ns, bool fast) {
-  int cap = std::max(fast ? VELAN_FAST_CAP : 8192, ((ns + 3) / 4) * 4 + 8 + (fast ? 40 : 0));
+  if (fast) return staging_need(ns, true) <= kFastCap ? kFastCap : kFastCapBig;
+  const int cap = std::max(8192, staging_need(ns, false));
   return (cap + 31) / 32 * 32;
 }
 
@@ -568,7 +586,9 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
     d_samples = D.bufs[B_SAMPLES].as<float>();
   }
 
-  const KernelChoice kc = choose_kernel(h.op, sc->variant, h.w);
+  const bool fast = sc->variant == VELAN_VARIANT_FAST;
+  const KernelChoice kc = choose_kernel(h.op, sc->variant, h.w,
+                                        fast && staging_cap(h.ns, true) != kFastCap);
   ScanParams p{};
   p.samples = d_samples;
   p.h2 = D.bufs[B_H2].as<float>();
@@ -594,8 +614,7 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
                ? (h.ns % 2 == 0)
                : (h.ns % 4 == 0) &&
                      (reinterpret_cast<uintptr_t>(d_samples) % 16 == 0);
-  const bool fast = sc->variant == VELAN_VARIANT_FAST;
-  p.cap = staging_cap(h.ns, fast);
+  p.cap = kc.cap ? kc.cap : staging_cap(h.ns, fast);
   if (fast) {
     // pairs then energies, 8 B per sample each
     D.bufs[B_EC].ensure(std::max<size_t>(1, static_cast<size_t>(L) * trace_floats * 16 + 64));

@@ -136,6 +136,33 @@ def test_window_lengths(engine, w, ns, variant):
         assert_close(r, ref, ns, len(v), 1e-6, sem_floor=2e-6 * M)
 
 
+@pytest.mark.parametrize("ns,w", [(2513, 15), (4001, 11), (5960, 21)])
+def test_long_traces_fast(engine, ns, w):
+    """Traces longer than the default FAST stage (2512 samples): the
+    large-stage kernel (one CTA per SM), through TMA (even ns) and the
+    synchronous fallback (odd ns), up to the FAST limit."""
+    rng = np.random.default_rng(ns)
+    G, M = 2, 6
+    samples = rng.uniform(-1, 1, (G, M, ns)).astype(np.float32)
+    coords = np.zeros((G, M, 4), np.float32)
+    coords[:, :, 2] = np.linspace(0, 3000, M)[None, :]
+    from paper_1907_11678_b200 import Dataset
+    ds = Dataset(samples, coords, np.full(G, M, np.int32), np.arange(G, dtype=np.uint32), 1000)
+    v = velocity_grid(1500.0, 4000.0, 5)
+    r = engine.run_cmp(ds, ScanConfig(w=w, velocities=v, kernel_variant="fast"), emit_matrix=True)
+    rng2 = np.random.default_rng(1)
+    rows = rng2.integers(0, G, 600).astype(np.int32)
+    ks = rng2.integers(0, ns, 600).astype(np.int32)
+    ref = oracle.run_cells(ds, "nmo", w, v, rows, ks, matrix=True)
+    got = r.values.reshape(G, ns, len(v))[rows, ks]
+    rep = oracle.compare(got, ref.matrix)
+    # U[-1, 1] noise: relative 1e-4 plus the 2e-6 * M semblance floor
+    err = np.abs(got.astype(np.float64) - ref.matrix)
+    assert np.all(err <= 1e-4 * np.abs(ref.matrix) + 2e-6 * M), rep
+    ex = engine.run_cmp(ds, ScanConfig(w=w, velocities=v, kernel_variant="exact"))
+    assert r.stats.naive_fetches == ex.stats.naive_fetches
+
+
 def test_hit_exact_matches_reference_rule():
     from paper_1907_11678_b200 import _native as N
     import ctypes as C
