@@ -26,4 +26,9 @@ clean:
 	rm -f $(LIB)
 	$(MAKE) -C oracle clean
 
-.PHONY: all lib oracle clean
+.PHONY: all lib oracle clean exp
+
+# experimental builds (not shipped): make exp NAME=s3 DEFS="-DVELAN_STAGES=3"
+exp:
+	@mkdir -p paper_1907_11678_b200/_lib/exp
+	$(NVCC) $(NVFLAGS) $(DEFS) -shared -o paper_1907_11678_b200/_lib/exp/lib$(NAME).so $(SRC) -lpthread 2> paper_1907_11678_b200/_lib/exp/$(NAME).log || (cat paper_1907_11678_b200/_lib/exp/$(NAME).log; exit 1)

@@ -81,7 +81,10 @@ struct KernelChoice {
 #define VELAN_FAST_CAP 2560
 #endif
 constexpr int kFastCap = VELAN_FAST_CAP;
-constexpr int kFastCapBig = 6016;  // ns <= 5968
+// large stages: kStages of them in ~190 KB (6016 entries, ns <= 5968, at
+// two stages)
+constexpr int kFastCapBig = (190 * 1024 / (kStages * 16)) / 32 * 32;
+constexpr int kFastMaxNs = kFastCapBig - 48;  // staging_need(ns) <= cap
 
 template <int OPK, int VAR, int WMAX, bool FIXED, int CAPF = 0>
 KernelChoice pick() {
@@ -196,10 +199,11 @@ void validate(const velan_gpu_dataset* ds, const velan_gpu_scan* sc,
     throw ApiError(VELAN_GPU_ECONFIG,
                    "scan_sweep: window does not fit trace length");
   // one trace must fit a staging stage (kStages stages per CTA)
-  if (ds->ns > (sc->variant == VELAN_VARIANT_FAST ? 5960 : 27000))
+  if (ds->ns > (sc->variant == VELAN_VARIANT_FAST ? kFastMaxNs : 27000))
     throw ApiError(VELAN_GPU_ECONFIG,
-                   "ns exceeds the shared-memory staging capacity of the "
-                   "kernel variant (FAST 5960, EXACT 27000 samples)");
+                   fmt("ns exceeds the shared-memory staging capacity of the "
+                       "kernel variant (FAST %lld, EXACT %lld samples)",
+                       kFastMaxNs, 27000));
   for (int g = 0; g < ds->n_gathers; ++g) {
     if (ds->ntraces[g] < 0 || ds->ntraces[g] > ds->max_traces)
       throw ApiError(VELAN_GPU_EPARAM,
