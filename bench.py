@@ -142,7 +142,10 @@ def load_traffic(workload: str):
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(workload)
+        e = d.get(workload)
+        # DRAM bytes (read + write) of the scan kernel per step, from the
+        # committed ncu launch list of the same command
+        return None if e is None else float(e["dram_bytes_per_step"])
     except Exception:
         return None
 
@@ -354,7 +357,12 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_reference_sample(wl, ds, args.cpu_seconds, os.cpu_count() or 1)
+            # same procedure as --impl reference: a 256-midpoint prefix of
+            # the line, one untimed warm-up sample (pages, threads), then the
+            # timed sample
+            ds_cpu = wl.spec.generate(count=min(G, 256))
+            cpu_reference_sample(wl, ds_cpu, 2.0, os.cpu_count() or 1)
+            cpu = cpu_reference_sample(wl, ds_cpu, args.cpu_seconds, os.cpu_count() or 1)
         except Exception as ex:  # reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "unavailable",
                    "sample": f"error: {ex}"}
