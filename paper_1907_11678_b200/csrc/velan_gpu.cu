@@ -73,6 +73,7 @@ struct KernelChoice {
   KernelFn fn = nullptr;
   int cc = 0;
   int cap = 0;  // compile-time stage capacity (FAST), 0 = runtime (EXACT)
+  size_t slot_bytes = 0;  // the kernel's plan slots (dynamic shared memory)
 };
 
 // FAST stage capacities (entries): the default, and the one for traces
@@ -92,7 +93,8 @@ KernelChoice pick() {
   // candidates per warp (the group of a CTA is kWarps x CC candidates)
   constexpr int CC = WMAX > 16 ? 1 : 2;
   constexpr int CAP = VAR == VAR_FAST ? (CAPF ? CAPF : kFastCap) : 0;
-  return KernelChoice{&semblance_scan_kernel<OPK, VAR, WMAX, FIXED, CC, CAP>, CC, CAP};
+  return KernelChoice{&semblance_scan_kernel<OPK, VAR, WMAX, FIXED, CC, CAP>, CC, CAP,
+                      2 * kStages * sizeof(PlanSlot<kWarps * CC, OpTraits<OPK>::NQ>)};
 }
 
 template <int OPK, int VAR>
@@ -649,7 +651,8 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
                              h.n_a + h.n_b + h.n_c;
   const size_t smem =
       (static_cast<size_t>(kStages) * p.cap * (fast ? 4 : 1) + meta_floats) *
-      sizeof(float);
+          sizeof(float) +
+      kc.slot_bytes;
   if (smem > 227 * 1024)
     throw ApiError(VELAN_GPU_ECONFIG,
                    "scan exceeds the 227 KB shared-memory budget of a CTA "
