@@ -73,7 +73,7 @@ struct KernelChoice {
   KernelFn fn = nullptr;
   int cc = 0;
   int cap = 0;  // compile-time stage capacity (FAST), 0 = runtime (EXACT)
-  size_t slot_bytes = 0;  // the kernel's plan slots (dynamic shared memory)
+  size_t slot_bytes = 0;  // plan slots + per-warp moveout terms (dynamic smem)
 };
 
 // FAST stage capacities (entries): the default, and the one for traces
@@ -94,7 +94,8 @@ KernelChoice pick() {
   constexpr int CC = WMAX > 16 ? 1 : 2;
   constexpr int CAP = VAR == VAR_FAST ? (CAPF ? CAPF : kFastCap) : 0;
   return KernelChoice{&semblance_scan_kernel<OPK, VAR, WMAX, FIXED, CC, CAP>, CC, CAP,
-                      2 * kStages * sizeof(PlanSlot<kWarps * CC, OpTraits<OPK>::NQ>)};
+                      2 * kStages * sizeof(PlanSlot) +
+                          sizeof(float) * kWarps * kBatch * CC * OpTraits<OPK>::NQ};
 }
 
 template <int OPK, int VAR>
