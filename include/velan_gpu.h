@@ -231,6 +231,57 @@ int velan_gpu_synth_generate(const velan_gpu_synth* p, float* samples,
                              float* coords, int32_t* ntraces,
                              uint32_t* cdp_id);
 
+/* ---------------------------------------------------------------------
+ * Files.  SSF1 trace files (read_dataset / write_dataset,
+ * io.hpp:88-166) and SMB1 pick files (write_picks, io.hpp:168-194), byte-
+ * compatible with the reference, read and written without materialising a
+ * Dataset of per-trace vectors.  Errors: ECONFIG = velan::format_error
+ * (message carries the byte offset), ERUNTIME = I/O failure, EPARAM = bad
+ * arguments.
+ * --------------------------------------------------------------------- */
+typedef struct velan_ssf1_info {
+  uint32_t n_gathers;      /* ncdps                                       */
+  uint32_t fold;           /* Dataset::fold (the layout's trace stride)    */
+  uint32_t ns, dt_us;      /* of the first gather                          */
+  int32_t uniform;         /* 1: every gather has the same ns and dt_us    */
+  uint64_t metadata_bytes; /* optional JSON tail                           */
+  uint64_t file_bytes;
+} velan_ssf1_info;
+
+typedef struct velan_ssf1 velan_ssf1;
+typedef struct velan_smb1_writer velan_smb1_writer;
+
+/* Index an SSF1 file: header words of every gather, validated like
+ * read_dataset (magic, version, trace count <= fold, dt != 0, metadata tail,
+ * no trailing bytes); samples are not read. */
+int velan_ssf1_open(const char* path, velan_ssf1** out, velan_ssf1_info* info);
+void velan_ssf1_close(velan_ssf1* f);
+/* Per-gather header arrays [n_gathers] (any pointer may be NULL). */
+int velan_ssf1_gathers(const velan_ssf1* f, uint32_t* cdp_id, int32_t* ntraces,
+                       uint32_t* ns, uint32_t* dt_us);
+int velan_ssf1_metadata(const velan_ssf1* f, char* buf, uint64_t cap);
+/* Gathers [first, first + count) into the flattened layout of
+ * velan_gpu_dataset: samples [count][max_traces][ns], coords
+ * [count][max_traces][4], zero beyond each gather's trace count.  One pread
+ * per gather, n_threads readers (0 = hardware concurrency); pass pinned
+ * buffers to feed asynchronous host->device copies. */
+int velan_ssf1_read(const velan_ssf1* f, int32_t first, int32_t count, int32_t max_traces,
+                    float* samples, float* coords, int32_t n_threads);
+/* write_dataset (io.hpp:95-122), byte-identical; samples must be host. */
+int velan_ssf1_write(const char* path, const velan_gpu_dataset* ds, const char* metadata,
+                     uint64_t metadata_bytes);
+
+/* write_picks (io.hpp:170-194) as a stream: the header declares n_cdps,
+ * records are appended block by block (per CDP: cdp_id, ns, nc, ns x
+ * (velocity, semblance), then the ns x nc matrix when with_matrix), and
+ * _end checks that every declared record was written. */
+int velan_smb1_begin(const char* path, uint32_t n_cdps, int32_t ns, int32_t nc,
+                     int32_t with_matrix, velan_smb1_writer** out);
+int velan_smb1_append(velan_smb1_writer* w, int32_t n, const uint32_t* cdp_id,
+                      const float* pick_velocity, const float* pick_semblance,
+                      const float* matrix);
+int velan_smb1_end(velan_smb1_writer* w);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

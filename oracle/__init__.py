@@ -94,6 +94,13 @@ def ref_lib() -> C.CDLL:
         lib.vref_finalize.argtypes = [_P, C.c_int, C.c_float, C.c_float, C.c_int, _P, _P]
         lib.vref_interpolate.restype = C.c_float
         lib.vref_interpolate.argtypes = [C.c_float, C.c_float, C.c_float]
+        lib.vref_write_dataset.restype = C.c_int
+        lib.vref_write_dataset.argtypes = [C.c_char_p, _P, _P, _P, _P, C.c_int, C.c_int,
+                                           C.c_int, C.c_uint32, C.c_char_p]
+        lib.vref_read_dataset.restype = C.c_int
+        lib.vref_read_dataset.argtypes = [C.c_char_p, _P, _P, _P, _P, _P, _P, _P]
+        lib.vref_write_picks.restype = C.c_int
+        lib.vref_write_picks.argtypes = [C.c_char_p, C.c_int, _P, C.c_int, C.c_int, _P, _P, _P]
         _ref = lib
     return _ref
 
@@ -259,3 +266,55 @@ def compare(run_matrix, ref_matrix):
             "mean_rel_err": float(rel.mean()) if rel.size else 0.0,
             "cells": int(rel.size), "argmax_mismatches": unexcused,
             "tie_excused": excused}
+
+
+# --------------------------------------------------------------------------
+# the reference's file formats (io.hpp), for byte-identity tests of the
+# native SSF1/SMB1 reader and writers
+
+def ref_write_dataset(ds, path: str, metadata: str = "") -> None:
+    """velan::write_dataset (io.hpp:95-122)."""
+    sm, co, nt, ids = _flat(ds)
+    G, M, ns = sm.shape
+    code = ref_lib().vref_write_dataset(str(path).encode(), _p(sm), _p(co), _p(nt), _p(ids),
+                                        G, M, ns, int(ds.dt_us), metadata.encode())
+    if code:
+        raise RuntimeError(ref_lib().vref_last_error().decode())
+
+
+def ref_read_dataset(path: str):
+    """velan::read_dataset (io.hpp:124-166) -> (samples, coords, ntraces,
+    cdp_id, dt_us, metadata); raises ValueError(format_error message)."""
+    lib = ref_lib()
+    dims = np.zeros(4, np.int32)
+    ml = C.c_uint64(0)
+    code = lib.vref_read_dataset(str(path).encode(), _p(dims), C.byref(ml), None, None, None,
+                                 None, None)
+    if code == 1:
+        raise ValueError(lib.vref_last_error().decode())
+    if code:
+        raise RuntimeError(lib.vref_last_error().decode())
+    G, M, ns, dt = (int(x) for x in dims)
+    sm = np.zeros((G, M, ns), np.float32)
+    co = np.zeros((G, M, 4), np.float32)
+    nt = np.zeros(G, np.int32)
+    ids = np.zeros(G, np.uint32)
+    meta = C.create_string_buffer(max(ml.value, 1))
+    code = lib.vref_read_dataset(str(path).encode(), _p(dims), C.byref(ml), _p(sm), _p(co),
+                                 _p(nt), _p(ids), meta)
+    if code:
+        raise RuntimeError(lib.vref_last_error().decode())
+    return sm, co, nt, ids, dt, meta.raw[:ml.value].decode()
+
+
+def ref_write_picks(path: str, cdp_id, velocity, semblance, nc: int, matrix=None) -> None:
+    """velan::write_picks (io.hpp:170-194)."""
+    ids = np.ascontiguousarray(cdp_id, np.uint32)
+    vel = np.ascontiguousarray(velocity, np.float32)
+    sem = np.ascontiguousarray(semblance, np.float32)
+    mat = None if matrix is None else np.ascontiguousarray(matrix, np.float32)
+    n, ns = vel.shape
+    code = ref_lib().vref_write_picks(str(path).encode(), n, _p(ids), ns, nc, _p(vel), _p(sem),
+                                      _p(mat))
+    if code:
+        raise RuntimeError(ref_lib().vref_last_error().decode())

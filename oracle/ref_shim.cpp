@@ -17,6 +17,8 @@
 //                                        crs_pipeline.hpp:162-180
 //   velan::oracle::semblance_reference   oracle.hpp:64-113
 //   velan::detail::parallel_for_indexed  cmp_pipeline.hpp:34-88
+//   velan::write_dataset / read_dataset / write_picks / read_picks
+//                                        io.hpp:95-224
 // For an arbitrary candidate list (BASELINE's slowness-linear grid) the
 // pairs are built exactly as scan_sweep builds them (scan.hpp:130-136) and
 // tiled with ScanConfig::effective_tile_size (scan.hpp:53-59); the per-pair
@@ -33,6 +35,7 @@
 
 #include "velan/cmp_pipeline.hpp"
 #include "velan/crs_pipeline.hpp"
+#include "velan/io.hpp"
 #include "velan/kernel.hpp"
 #include "velan/oracle.hpp"
 #include "velan/scan.hpp"
@@ -357,6 +360,94 @@ void vref_finalize(const float* num, int w, float den, float ac, int m_used,
 
 float vref_interpolate(float a, float b, float x) {
   return velan::interpolate(a, b, x);
+}
+
+// velan::write_dataset (io.hpp:95-122) of a flattened dataset.  Returns 0
+// ok, 2 parameter_error, 3 error (messages via vref_last_error).
+int vref_write_dataset(const char* path, const float* samples, const float* coords,
+                       const int32_t* ntraces, const uint32_t* cdp_id, int G, int M,
+                       int ns, uint32_t dt_us, const char* metadata) {
+  try {
+    velan::Dataset ds = make_dataset(samples, coords, ntraces, cdp_id, G, M, ns, dt_us);
+    if (metadata) ds.metadata_json = metadata;
+    velan::write_dataset(ds, path);
+    return 0;
+  } catch (const velan::parameter_error& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 3;
+  }
+}
+
+// velan::read_dataset (io.hpp:124-166): dims first (out4 = ncdps, fold, ns,
+// dt_us of gather 0; metadata length in *meta_len), then, with buffers, the
+// flattened arrays.  Returns 0 ok, 1 format_error, 3 error.
+int vref_read_dataset(const char* path, int32_t* out4, uint64_t* meta_len, float* samples,
+                      float* coords, int32_t* ntraces, uint32_t* cdp_id, char* metadata) {
+  try {
+    const velan::Dataset ds = velan::read_dataset(path);
+    const int G = static_cast<int>(ds.ncdps());
+    const int M = static_cast<int>(ds.fold);
+    const int ns = G ? static_cast<int>(ds.gathers[0].ns) : 0;
+    out4[0] = G;
+    out4[1] = M;
+    out4[2] = ns;
+    out4[3] = G ? static_cast<int32_t>(ds.gathers[0].dt_us) : 0;
+    if (meta_len) *meta_len = ds.metadata_json.size();
+    if (!samples) return 0;
+    for (int g = 0; g < G; ++g) {
+      const velan::CdpGather& cg = ds.gathers[g];
+      cdp_id[g] = cg.cdp_id;
+      ntraces[g] = static_cast<int32_t>(cg.traces.size());
+      for (size_t m = 0; m < cg.traces.size(); ++m) {
+        const velan::Trace& t = cg.traces[m];
+        float* c4 = coords + (static_cast<size_t>(g) * M + m) * 4;
+        c4[0] = t.sx;
+        c4[1] = t.sy;
+        c4[2] = t.gx;
+        c4[3] = t.gy;
+        std::memcpy(samples + (static_cast<size_t>(g) * M + m) * ns, t.samples.data(),
+                    sizeof(float) * ns);
+      }
+    }
+    if (metadata) std::memcpy(metadata, ds.metadata_json.data(), ds.metadata_json.size());
+    return 0;
+  } catch (const velan::format_error& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 3;
+  }
+}
+
+// velan::write_picks (io.hpp:170-194) of n records built from flat arrays.
+int vref_write_picks(const char* path, int n, const uint32_t* cdp_id, int ns, int nc,
+                     const float* velocity, const float* semblance, const float* matrix) {
+  try {
+    std::vector<velan::SemblanceMatrix> res(n);
+    for (int r = 0; r < n; ++r) {
+      velan::SemblanceMatrix& m = res[r];
+      m.cdp_id = cdp_id[r];
+      m.ns = ns;
+      m.nc = nc;
+      m.best_velocity.resize(ns);
+      for (int k = 0; k < ns; ++k) {
+        m.best_velocity[k].velocity = velocity[static_cast<size_t>(r) * ns + k];
+        m.best_velocity[k].semblance = semblance[static_cast<size_t>(r) * ns + k];
+      }
+      if (matrix)
+        m.values.assign(matrix + static_cast<size_t>(r) * ns * nc,
+                        matrix + static_cast<size_t>(r + 1) * ns * nc);
+    }
+    velan::write_picks(res, path, matrix != nullptr);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 3;
+  }
 }
 
 }  // extern "C"

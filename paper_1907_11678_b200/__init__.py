@@ -28,11 +28,22 @@ from .api import (  # noqa: F401
     velocity_grid,
 )
 from . import configs  # noqa: F401
+from .files import (  # noqa: F401
+    FormatError,
+    SMB1Writer,
+    SSF1Reader,
+    read_smb1,
+    read_ssf1,
+    run_cmp_file,
+    write_smb1,
+    write_ssf1,
+)
 
 __all__ = [
     "CacheStats", "ConfigError", "CrsAbcGrid", "Dataset", "DeviceError",
     "Engine", "ParameterError", "Plan", "ScanConfig", "ScanResult",
     "VelanError", "describe", "device_count", "neighbors_of", "run_cmp", "run_crs",
     "scan_cdp", "scan_central_cdp", "slowness_grid", "velocity_grid",
-    "configs",
+    "configs", "FormatError", "SMB1Writer", "SSF1Reader", "read_smb1", "read_ssf1",
+    "run_cmp_file", "write_smb1", "write_ssf1",
 ]

@@ -98,6 +98,18 @@ class Synth(C.Structure):
     ]
 
 
+class SSF1Info(C.Structure):
+    _fields_ = [
+        ("n_gathers", C.c_uint32),
+        ("fold", C.c_uint32),
+        ("ns", C.c_uint32),
+        ("dt_us", C.c_uint32),
+        ("uniform", C.c_int32),
+        ("metadata_bytes", C.c_uint64),
+        ("file_bytes", C.c_uint64),
+    ]
+
+
 # Every symbol include/velan_gpu.h declares, with its ctypes signature.
 _P = C.c_void_p
 SIGNATURES = {
@@ -119,6 +131,16 @@ SIGNATURES = {
     "velan_gpu_hit_batch": (C.c_int, [_P, C.c_int32, C.c_double, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P]),
     "velan_gpu_synth_generate": (C.c_int, [C.POINTER(Synth), _P, _P, _P, _P]),
     "velan_gpu_measure_fp32_peak": (C.c_int, [C.c_int32, C.POINTER(C.c_double)]),
+    "velan_ssf1_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(SSF1Info)]),
+    "velan_ssf1_close": (None, [_P]),
+    "velan_ssf1_gathers": (C.c_int, [_P, _P, _P, _P, _P]),
+    "velan_ssf1_metadata": (C.c_int, [_P, _P, C.c_uint64]),
+    "velan_ssf1_read": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P, _P, C.c_int32]),
+    "velan_ssf1_write": (C.c_int, [C.c_char_p, C.POINTER(Dataset), C.c_char_p, C.c_uint64]),
+    "velan_smb1_begin": (C.c_int, [C.c_char_p, C.c_uint32, C.c_int32, C.c_int32, C.c_int32,
+                                   C.POINTER(C.c_void_p)]),
+    "velan_smb1_append": (C.c_int, [_P, C.c_int32, _P, _P, _P, _P]),
+    "velan_smb1_end": (C.c_int, [_P]),
 }
 
 _lib = None

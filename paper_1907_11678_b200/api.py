@@ -248,6 +248,7 @@ class ScanResult:
     stats: CacheStats = field(default_factory=CacheStats)
     kernel_ms: float = 0.0
     total_ms: float = 0.0
+    n_candidates: int = 0  # flat candidate count (SemblanceMatrix::nc)
 
     @property
     def best_velocity(self) -> np.ndarray:
@@ -374,7 +375,7 @@ class Engine:
                           ds.cdp_id[rows] if G else ds.cdp_id, mat,
                           CacheStats(int(res.valid_intersections),
                                      int(res.nominal_intersections)),
-                          float(res.kernel_ms), float(res.total_ms))
+                          float(res.kernel_ms), float(res.total_ms), int(ncand))
 
     def run_cmp(self, ds: Dataset, config: ScanConfig,
                 emit_matrix: bool = False, out=None, rows=None) -> ScanResult:

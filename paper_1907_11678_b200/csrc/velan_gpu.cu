@@ -768,6 +768,11 @@ struct velan_gpu_plan {
   int launches = 0;
 };
 
+// the thread's last-error message, shared with ssf_io.cpp
+namespace velan_gpu {
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace velan_gpu
+
 #define VG_API_BEGIN try {
 #define VG_API_END                                    \
   }                                                   \
