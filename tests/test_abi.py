@@ -20,7 +20,7 @@ HEADER = os.path.join(ROOT, "include", "velan_gpu.h")
 def declared_functions():
     text = open(HEADER).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(velan_gpu_[a-z0-9_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(velan_(?:gpu|ssf1|smb1)_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_declares_the_expected_surface():
