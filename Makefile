@@ -8,7 +8,8 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xptxas -v \
            -Xcompiler -fPIC,-ffp-contract=off,-O3 -Iinclude
 LIB := paper_1907_11678_b200/_lib/libvelan_gpu.so
 SRC := paper_1907_11678_b200/csrc/velan_gpu.cu paper_1907_11678_b200/csrc/synth.cpp \
-       paper_1907_11678_b200/csrc/peak.cu paper_1907_11678_b200/csrc/ssf_io.cpp
+       paper_1907_11678_b200/csrc/peak.cu paper_1907_11678_b200/csrc/ssf_io.cpp \
+       paper_1907_11678_b200/csrc/synth_gpu.cu
 HDR := paper_1907_11678_b200/csrc/semblance_kernels.cuh include/velan_gpu.h
 
 all: lib oracle

@@ -230,6 +230,14 @@ typedef struct velan_gpu_synth {
 int velan_gpu_synth_generate(const velan_gpu_synth* p, float* samples,
                              float* coords, int32_t* ntraces,
                              uint32_t* cdp_id);
+/* The same generator on the device: fills device memory
+ * d_samples [n_gathers][n_traces][ns] on `stream` (a cudaStream_t, NULL =
+ * default) with the host generator's streams and model (geometry via
+ * velan_gpu_synth_generate with samples = NULL).  Synchronous. */
+int velan_gpu_synth_generate_device(const velan_gpu_synth* p, float* d_samples,
+                                    void* stream);
+/* The CRS line's reflectors, 6 doubles per event (t0, v, amp, x, A, B). */
+int velan_gpu_synth_line_events(const velan_gpu_synth* p, double* out6);
 
 /* ---------------------------------------------------------------------
  * Files.  SSF1 trace files (read_dataset / write_dataset,

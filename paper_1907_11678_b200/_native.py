@@ -130,6 +130,8 @@ SIGNATURES = {
     "velan_gpu_plan_destroy": (None, [_P]),
     "velan_gpu_hit_batch": (C.c_int, [_P, C.c_int32, C.c_double, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P]),
     "velan_gpu_synth_generate": (C.c_int, [C.POINTER(Synth), _P, _P, _P, _P]),
+    "velan_gpu_synth_generate_device": (C.c_int, [C.POINTER(Synth), _P, _P]),
+    "velan_gpu_synth_line_events": (C.c_int, [C.POINTER(Synth), _P]),
     "velan_gpu_measure_fp32_peak": (C.c_int, [C.c_int32, C.POINTER(C.c_double)]),
     "velan_ssf1_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(SSF1Info)]),
     "velan_ssf1_close": (None, [_P]),

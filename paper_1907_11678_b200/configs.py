@@ -47,11 +47,7 @@ class SynthSpec:
     b_max: float = 1e-7
     seed: int = 11678
 
-    def generate(self, first: int = 0, count: Optional[int] = None,
-                 n_threads: int = 0, n_line: Optional[int] = None) -> Dataset:
-        """Gathers [first, first + count) of the full line."""
-        lib = N.load()
-        count = self.n_gathers if count is None else count
+    def _struct(self, first: int, count: int, n_threads: int, n_line: Optional[int]):
         s = N.Synth()
         for f, _ in N.Synth._fields_:
             if hasattr(self, f):
@@ -60,6 +56,40 @@ class SynthSpec:
         s.gather_first = first
         s.n_threads = n_threads
         s.n_line = self.n_gathers if n_line is None else n_line
+        return s
+
+    def generate_device(self, first: int = 0, count: Optional[int] = None,
+                        n_line: Optional[int] = None, device: int = 0) -> Dataset:
+        """Gathers [first, first + count) generated in HBM by the device
+        generator (synth_gpu.cu): samples is a CUDA tensor, the geometry
+        comes from the host generator (no samples)."""
+        import torch
+        lib = N.load()
+        count = self.n_gathers if count is None else count
+        s = self._struct(first, count, 0, n_line)
+        samples = torch.empty((count, self.n_traces, self.ns), dtype=torch.float32,
+                              device=f"cuda:{device}")
+        coords = np.empty((count, self.n_traces, 4), np.float32)
+        ntr = np.empty(count, np.int32)
+        ids = np.empty(count, np.uint32)
+        if lib.velan_gpu_synth_generate(C.byref(s), None, coords.ctypes.data,
+                                        ntr.ctypes.data, ids.ctypes.data) != 0:
+            raise ParameterError("velan_gpu_synth_generate: bad parameters")
+        with torch.cuda.device(device):
+            stream = torch.cuda.current_stream().cuda_stream
+            if lib.velan_gpu_synth_generate_device(C.byref(s), samples.data_ptr(), stream) != 0:
+                raise ParameterError("velan_gpu_synth_generate_device: bad parameters or "
+                                     "device failure")
+        return Dataset(samples, coords, ntr, ids, self.dt_us,
+                       {"generator": "velan_gpu synth (device)", "spec": self.__dict__.copy(),
+                        "first": first})
+
+    def generate(self, first: int = 0, count: Optional[int] = None,
+                 n_threads: int = 0, n_line: Optional[int] = None) -> Dataset:
+        """Gathers [first, first + count) of the full line."""
+        lib = N.load()
+        count = self.n_gathers if count is None else count
+        s = self._struct(first, count, n_threads, n_line)
         samples = np.empty((count, self.n_traces, self.ns), np.float32)
         coords = np.empty((count, self.n_traces, 4), np.float32)
         ntr = np.empty(count, np.int32)

@@ -56,12 +56,48 @@ void add_event(float* tr, int ns, double dt, double t, double amp,
     tr[s] += static_cast<float>(amp * ricker(s * dt - t, freq));
 }
 
+// CRS: reflectors are global to the line, one stream
+std::vector<Event> make_line_events(const velan_gpu_synth* p, int n_line) {
+  std::vector<Event> line_events;
+  Stream es(mix64(p->seed ^ 0xC0FFEE1234ull));
+  const double L = (n_line - 1) * p->spacing;
+  for (int e = 0; e < p->n_events; ++e) {
+    Event ev;
+    ev.x = es.uniform(0.0, L);
+    ev.t0 = es.uniform(p->t0_lo, p->t0_hi);
+    ev.A = es.uniform(-p->a_abs, p->a_abs);
+    ev.B = es.uniform(0.0, p->b_max);
+    ev.v = es.uniform(p->v_lo, p->v_hi);
+    ev.amp = es.uniform(p->amp_lo, p->amp_hi);
+    line_events.push_back(ev);
+  }
+  return line_events;
+}
+
 }  // namespace
+
+// The line's reflectors as (t0, v, amp, x, A, B) per event, for the device
+// generator (synth_gpu.cu).
+extern "C" int velan_gpu_synth_line_events(const velan_gpu_synth* p, double* out6) {
+  if (!p || !out6) return VELAN_GPU_EPARAM;
+  const int n_line = p->n_line > 0 ? p->n_line : p->gather_first + p->n_gathers;
+  const std::vector<Event> ev = make_line_events(p, n_line);
+  for (size_t e = 0; e < ev.size(); ++e) {
+    out6[6 * e + 0] = ev[e].t0;
+    out6[6 * e + 1] = ev[e].v;
+    out6[6 * e + 2] = ev[e].amp;
+    out6[6 * e + 3] = ev[e].x;
+    out6[6 * e + 4] = ev[e].A;
+    out6[6 * e + 5] = ev[e].B;
+  }
+  return VELAN_GPU_OK;
+}
 
 extern "C" int velan_gpu_synth_generate(const velan_gpu_synth* p,
                                         float* samples, float* coords,
                                         int32_t* ntraces, uint32_t* cdp_id) {
-  if (!p || !samples || !coords || !ntraces || !cdp_id) return VELAN_GPU_EPARAM;
+  // samples may be NULL: geometry only (the device generator fills samples)
+  if (!p || !coords || !ntraces || !cdp_id) return VELAN_GPU_EPARAM;
   if (p->n_gathers < 0 || p->n_traces < 1 || p->ns < 2 || p->dt_us == 0 ||
       p->freq <= 0.0 || p->n_events < 0)
     return VELAN_GPU_EPARAM;
@@ -69,22 +105,8 @@ extern "C" int velan_gpu_synth_generate(const velan_gpu_synth* p,
   const double dt = static_cast<double>(p->dt_us) * 1e-6;
   const int n_line = p->n_line > 0 ? p->n_line : p->gather_first + G;
 
-  // CRS: reflectors are global to the line
   std::vector<Event> line_events;
-  if (p->kind == 1) {
-    Stream es(mix64(p->seed ^ 0xC0FFEE1234ull));
-    const double L = (n_line - 1) * p->spacing;
-    for (int e = 0; e < p->n_events; ++e) {
-      Event ev;
-      ev.x = es.uniform(0.0, L);
-      ev.t0 = es.uniform(p->t0_lo, p->t0_hi);
-      ev.A = es.uniform(-p->a_abs, p->a_abs);
-      ev.B = es.uniform(0.0, p->b_max);
-      ev.v = es.uniform(p->v_lo, p->v_hi);
-      ev.amp = es.uniform(p->amp_lo, p->amp_hi);
-      line_events.push_back(ev);
-    }
-  }
+  if (p->kind == 1) line_events = make_line_events(p, n_line);
 
   auto gen_gather = [&](int gl) {
     const int g = p->gather_first + gl;
@@ -113,6 +135,7 @@ extern "C" int velan_gpu_synth_generate(const velan_gpu_synth* p,
       c4[1] = 0.0f;
       c4[2] = static_cast<float>(mx + h);
       c4[3] = 0.0f;
+      if (!samples) continue;
       float* tr = samples + (static_cast<size_t>(gl) * M + m) * ns;
       std::fill(tr, tr + ns, 0.0f);
       if (p->kind == 0) {
