@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define VELAN_GPU_ABI_VERSION 1
+#define VELAN_GPU_ABI_VERSION 2
 
 /* Status codes.  0 = success.  Config and parameter errors are raised before
  * any device work, like ScanConfig::validate (scan.hpp:61-78). */
@@ -126,6 +126,14 @@ typedef struct velan_gpu_result {
   uint64_t nominal_intersections; /* rows * ns * n_cand * traces/sweep  */
   double kernel_ms;  /* device time of the scan kernels, max over devices */
   double total_ms;   /* wall time of the whole call                       */
+  /* Optional per-sample top-k (QC of the semblance panel
+   * without the ns x n_cand matrix): the k best candidates of every output
+   * sample, best first (ties: lower flat index first, so entry 0 is the
+   * pick); entries past n_cand hold index -1.  topk 0 = off, max 8.  Same
+   * memory kind as the other outputs (out_mem). */
+  int32_t topk;
+  int32_t* topk_idx;      /* [rows][ns][topk] flat candidate index      */
+  float* topk_semblance;  /* [rows][ns][topk]                           */
 } velan_gpu_result;
 
 typedef struct velan_gpu_ctx velan_gpu_ctx;

@@ -63,6 +63,9 @@ class Result(C.Structure):
         ("nominal_intersections", C.c_uint64),
         ("kernel_ms", C.c_double),
         ("total_ms", C.c_double),
+        ("topk", C.c_int32),
+        ("topk_idx", C.c_void_p),
+        ("topk_semblance", C.c_void_p),
     ]
 
 

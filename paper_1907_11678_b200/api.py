@@ -249,6 +249,8 @@ class ScanResult:
     kernel_ms: float = 0.0
     total_ms: float = 0.0
     n_candidates: int = 0  # flat candidate count (SemblanceMatrix::nc)
+    topk_idx: Optional[np.ndarray] = None        # [rows, ns, k], best first
+    topk_semblance: Optional[np.ndarray] = None  # [rows, ns, k]
 
     @property
     def best_velocity(self) -> np.ndarray:
@@ -341,7 +343,7 @@ class Engine:
 
     def _run(self, fn, ds: Dataset, op: int, variant: str, w: int,
              v: np.ndarray, abc: Optional[CrsAbcGrid], apm: float,
-             emit_matrix: bool, out=None, rows=None) -> ScanResult:
+             emit_matrix: bool, out=None, rows=None, topk: int = 0) -> ScanResult:
         lib = N.load()
         keep: list = []
         sc = _scan_struct(op, variant, w, v, abc, apm, keep, rows)
@@ -357,7 +359,12 @@ class Engine:
             best_st = np.zeros((G, ns), np.float32)
         rows = np.zeros(G, np.int32)
         mat = np.zeros((G, ns, ncand), np.float32) if emit_matrix else None
+        tki = np.zeros((G, ns, topk), np.int32) if topk else None
+        tks = np.zeros((G, ns, topk), np.float32) if topk else None
         res = N.Result()
+        res.topk = topk
+        res.topk_idx = _ptr(tki)
+        res.topk_semblance = _ptr(tks)
         res.out_mem = N.MEM_HOST
         res.best_idx = _ptr(best_idx)
         res.best_semblance = _ptr(best_s)
@@ -375,26 +382,29 @@ class Engine:
                           ds.cdp_id[rows] if G else ds.cdp_id, mat,
                           CacheStats(int(res.valid_intersections),
                                      int(res.nominal_intersections)),
-                          float(res.kernel_ms), float(res.total_ms), int(ncand))
+                          float(res.kernel_ms), float(res.total_ms), int(ncand), tki, tks)
 
     def run_cmp(self, ds: Dataset, config: ScanConfig,
-                emit_matrix: bool = False, out=None, rows=None) -> ScanResult:
-        """``rows`` = (first, count) restricts the outputs to a row block."""
+                emit_matrix: bool = False, out=None, rows=None,
+                topk: int = 0) -> ScanResult:
+        """``rows`` = (first, count) restricts the outputs to a row block;
+        ``topk`` (<= 8) adds the k best candidates of every sample."""
         config.validate()
         return self._run(N.load().velan_gpu_cmp, ds, N.OP_NMO,
                          config.kernel_variant, config.w, config.grid(), None,
-                         0.0, emit_matrix, out, rows)
+                         0.0, emit_matrix, out, rows, topk)
 
     def run_crs(self, ds: Dataset, config: ScanConfig, apm: float,
                 abc: Optional[CrsAbcGrid] = None,
-                emit_matrix: bool = False, out=None, rows=None) -> ScanResult:
+                emit_matrix: bool = False, out=None, rows=None,
+                topk: int = 0) -> ScanResult:
         """``rows`` = (first, count): a shard's own block of the cdp_id-ordered
         rows; the remaining gathers are halo feeding the neighbourhoods."""
         config.validate()
         op = N.OP_CRS_ABC if abc is not None else N.OP_CRS_D2
         return self._run(N.load().velan_gpu_crs, ds, op, config.kernel_variant,
                          config.w, config.grid(), abc, apm, emit_matrix, out,
-                         rows)
+                         rows, topk)
 
     def plan(self, ds: Dataset, config: ScanConfig, op: str = "nmo",
              apm: float = 0.0, abc: Optional[CrsAbcGrid] = None,

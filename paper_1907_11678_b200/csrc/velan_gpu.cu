@@ -384,7 +384,7 @@ struct DevBuf {
 
 enum BufId {
   B_SAMPLES, B_EC, B_H2, B_NTR, B_LEGOFF, B_LEGG, B_LEGD2, B_LEGDM, B_T0, B_A, B_B,
-  B_V, B_BIDX, B_BS, B_BST, B_MAT, B_VALID, B_COUNT
+  B_V, B_BIDX, B_BS, B_BST, B_MAT, B_VALID, B_TKI, B_TKS, B_COUNT
 };
 
 struct DeviceState {
@@ -525,6 +525,13 @@ int staging_cap(int ns, bool fast) {
   return (cap + 31) / 32 * 32;
 }
 
+void check_topk(const velan_gpu_result* res) {
+  if (res->topk < 0 || res->topk > 8)
+    throw ApiError(VELAN_GPU_EPARAM, "topk must be in [0, 8]");
+  if (res->topk > 0 && (!res->topk_idx || !res->topk_semblance))
+    throw ApiError(VELAN_GPU_EPARAM, "topk output arrays are null");
+}
+
 struct RunOut {
   uint64_t valid = 0;
   double kernel_ms = 0.0;
@@ -563,7 +570,16 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
   const size_t cells = static_cast<size_t>(rows) * h.ns;
   int32_t* d_bidx;
   float *d_bs, *d_bst, *d_mat = nullptr;
+  const int K = res->topk;
+  int32_t* d_tki = nullptr;
+  float* d_tks = nullptr;
   if (out_host) {
+    if (K > 0) {
+      D.bufs[B_TKI].ensure(cells * K * 4);
+      D.bufs[B_TKS].ensure(cells * K * 4);
+      d_tki = D.bufs[B_TKI].as<int32_t>();
+      d_tks = D.bufs[B_TKS].as<float>();
+    }
     D.bufs[B_BIDX].ensure(cells * 4);
     D.bufs[B_BS].ensure(cells * 4);
     D.bufs[B_BST].ensure(cells * 4);
@@ -580,6 +596,15 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
     d_bst = res->best_stack + static_cast<size_t>(s.r0) * h.ns;
     if (res->matrix)
       d_mat = res->matrix + static_cast<size_t>(s.r0) * h.ns * h.ncand;
+    if (K > 0) {
+      d_tki = res->topk_idx + static_cast<size_t>(s.r0) * h.ns * K;
+      d_tks = res->topk_semblance + static_cast<size_t>(s.r0) * h.ns * K;
+    }
+  }
+  if (K > 0 && !d_mat) {
+    // top-k reads the semblance panel from HBM: an internal matrix buffer
+    D.bufs[B_MAT].ensure(cells * h.ncand * 4);
+    d_mat = D.bufs[B_MAT].as<float>();
   }
   D.bufs[B_VALID].ensure(8);
   VG_CUDA(cudaMemsetAsync(D.bufs[B_VALID].p, 0, 8, st));
@@ -703,6 +728,13 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
     VG_CUDA(cudaEventRecord(D.ev(2 * wv + 1), st));
     ++out.launches;
   }
+  if (K > 0 && cells > 0) {
+    const long long nc = static_cast<long long>(cells);
+    topk_kernel<<<static_cast<unsigned>((nc + 7) / 8), 256, 0, st>>>(d_mat, nc, h.ncand, K,
+                                                                     d_tks, d_tki);
+    VG_CUDA(cudaGetLastError());
+    ++out.launches;
+  }
   unsigned long long valid = 0;
   VG_CUDA(cudaMemcpyAsync(&valid, D.bufs[B_VALID].p, 8, cudaMemcpyDeviceToHost,
                           st));
@@ -717,6 +749,12 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
       VG_CUDA(cudaMemcpyAsync(
           res->matrix + static_cast<size_t>(s.r0) * h.ns * h.ncand, d_mat,
           cells * h.ncand * 4, cudaMemcpyDeviceToHost, st));
+    if (K > 0) {
+      VG_CUDA(cudaMemcpyAsync(res->topk_idx + static_cast<size_t>(s.r0) * h.ns * K, d_tki,
+                              cells * K * 4, cudaMemcpyDeviceToHost, st));
+      VG_CUDA(cudaMemcpyAsync(res->topk_semblance + static_cast<size_t>(s.r0) * h.ns * K,
+                              d_tks, cells * K * 4, cudaMemcpyDeviceToHost, st));
+    }
   }
   VG_CUDA(cudaStreamSynchronize(st));
   out.valid = valid;
@@ -802,7 +840,7 @@ int velan_gpu_abi_layout(int32_t* out8) {
   out8[2] = sizeof(velan_gpu_scan);
   out8[3] = offsetof(velan_gpu_scan, row_count);
   out8[4] = sizeof(velan_gpu_result);
-  out8[5] = offsetof(velan_gpu_result, total_ms);
+  out8[5] = offsetof(velan_gpu_result, topk_semblance);
   out8[6] = sizeof(velan_gpu_synth);
   out8[7] = offsetof(velan_gpu_synth, n_threads);
   return VELAN_GPU_OK;
@@ -915,6 +953,7 @@ static int run_oneshot(velan_gpu_ctx* ctx, const velan_gpu_dataset* ds,
   }
   if (!res->best_idx || !res->best_semblance || !res->best_stack)
     throw ApiError(VELAN_GPU_EPARAM, "result arrays are null");
+  check_topk(res);
   if (ds->samples_mem == VELAN_MEM_DEVICE && ctx->devs.size() != 1)
     throw ApiError(VELAN_GPU_ECONFIG,
                    "device-resident samples need a single-device context");
@@ -1047,6 +1086,7 @@ int velan_gpu_plan_execute(velan_gpu_plan* plan, velan_gpu_result* res,
   if (plan->h.rows == 0) return VELAN_GPU_OK;
   if (!res->best_idx || !res->best_semblance || !res->best_stack)
     throw ApiError(VELAN_GPU_EPARAM, "result arrays are null");
+  check_topk(res);
   const RunOut o =
       run_shard(plan->dev, plan->h, plan->shard, &plan->ds, &plan->sc, res,
                 plan->d_samples_ext, static_cast<cudaStream_t>(stream), true,

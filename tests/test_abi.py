@@ -53,7 +53,7 @@ def test_library_is_sm100a_only():
 
 
 def test_abi_version():
-    assert N.load().velan_gpu_abi_version() == 1
+    assert N.load().velan_gpu_abi_version() == 2
 
 
 def test_struct_layouts_match_ctypes():
@@ -61,7 +61,7 @@ def test_struct_layouts_match_ctypes():
     assert N.load().velan_gpu_abi_layout(out.ctypes.data) == 0
     expect = [C.sizeof(N.Dataset), N.Dataset.samples_device.offset,
               C.sizeof(N.Scan), N.Scan.row_count.offset,
-              C.sizeof(N.Result), N.Result.total_ms.offset,
+              C.sizeof(N.Result), N.Result.topk_semblance.offset,
               C.sizeof(N.Synth), N.Synth.n_threads.offset]
     assert list(out) == expect
 

@@ -218,3 +218,32 @@ def test_run_crs_matches_reference_pipeline(engine):
     np.testing.assert_array_equal(r.best_idx, ref.best_idx)
     np.testing.assert_array_equal(bits(r.stack_trace), bits(ref.best_stack))
     assert r.stats.naive_fetches == ref.valid
+
+
+@pytest.mark.parametrize("variant,k", [("exact", 1), ("exact", 5), ("fast", 8)])
+def test_topk_matches_matrix(engine, variant, k):
+    """Per-sample top-k (§8f-2) equals the k best entries of the full matrix
+    (best first, ties to the lower flat index); entry 0 is the pick."""
+    wl = configs.crs_small()
+    ds = wl.spec.generate(count=12)
+    grid = CrsAbcGrid(np.linspace(-2e-4, 2e-4, 3), np.linspace(0, 1e-7, 2),
+                      np.linspace(1500, 3500, 5))
+    cfg = ScanConfig(w=11, velocities=grid.v, kernel_variant=variant)
+    r = engine.run_crs(ds, cfg, 125.0, abc=grid, emit_matrix=True, topk=k)
+    m = r.values.reshape(-1, grid.ncand)
+    # reference order: descending semblance, ascending index among equals
+    order = np.lexsort((np.broadcast_to(np.arange(grid.ncand), m.shape), -m), axis=1)[:, :k]
+    ti = r.topk_idx.reshape(-1, k)
+    ts = r.topk_semblance.reshape(-1, k)
+    np.testing.assert_array_equal(ti, order)
+    np.testing.assert_array_equal(ts, np.take_along_axis(m, order, axis=1))
+    np.testing.assert_array_equal(ti[:, 0], r.best_idx.reshape(-1))
+
+
+def test_topk_more_than_candidates(engine, cmp_small):
+    """k > n_cand: the tail entries are index -1."""
+    ds = cmp_small[1].subset(range(2))
+    cfg = ScanConfig(w=11, velocities=velocity_grid(1500.0, 3000.0, 3))
+    r = engine.run_cmp(ds, cfg, topk=5)
+    assert np.all(r.topk_idx[..., 3:] == -1)
+    assert np.all(np.sort(r.topk_idx[..., :3], axis=-1) == np.arange(3))
