@@ -251,12 +251,17 @@ def _blocks(n: int, block: int) -> Iterable[tuple]:
 
 def run_cmp_file(engine: Engine, ssf_path: str, config: ScanConfig,
                  smb_path: Optional[str] = None, block: int = 1024,
-                 threads: int = 0, keep_results: bool = True):
+                 threads: int = 0, keep_results: bool = True,
+                 include_matrix: bool = False, topk: int = 0):
     """run_cmp over an SSF1 file in gather blocks: a reader thread fills the
     next pinned block while the GPU scans the current one (the ctypes call
     releases the GIL), and the picks of each block are appended to the
-    SMB1 file as soon as they are back.  Returns the per-block ScanResults
-    (or only the totals when keep_results is False)."""
+    SMB1 file as soon as they are back.  ``include_matrix`` streams the
+    full ns x n_cand panels into the SMB1 records block by block (SMB1's
+    flagged matrices, io.hpp:170-194) without holding the line's matrix;
+    ``topk`` keeps the k best candidates per sample in the results.
+    Returns the per-block ScanResults (or only the totals when keep_results
+    is False)."""
     config.validate()
     with SSF1Reader(ssf_path) as rd:
         if not rd.uniform:
@@ -264,7 +269,8 @@ def run_cmp_file(engine: Engine, ssf_path: str, config: ScanConfig,
         G = rd.n_gathers
         bufs = [(_alloc((block, rd.fold, rd.ns), np.float32, True),
                  _alloc((block, rd.fold, 4), np.float32, True)) for _ in range(2)]
-        writer = SMB1Writer(smb_path, G, rd.ns, len(config.grid())) if smb_path else None
+        writer = (SMB1Writer(smb_path, G, rd.ns, len(config.grid()), include_matrix)
+                  if smb_path else None)
         results = []
         valid = 0
         kernel_ms = 0.0
@@ -290,12 +296,14 @@ def run_cmp_file(engine: Engine, ssf_path: str, config: ScanConfig,
                 if i + 1 < len(blocks):  # prefetch into the other buffer
                     th = threading.Thread(target=load, args=(i + 1,))
                     th.start()
-                r = engine.run_cmp(ds, config)
+                r = engine.run_cmp(ds, config, emit_matrix=include_matrix, topk=topk)
                 valid += r.stats.naive_fetches
                 kernel_ms += r.kernel_ms
                 if writer is not None:
                     writer.append_result(r)
                 if keep_results:
+                    if include_matrix and smb_path:
+                        r.values = None  # already on disk
                     results.append(r)
             if writer is not None:
                 writer.close()

@@ -216,3 +216,25 @@ def test_run_cmp_file_streams_like_in_memory(engine, tmp_path):
     write_smb1(ref, whole)
     assert out.read_bytes() == whole.read_bytes()
     assert sum(b.stats.naive_fetches for b in blocks) == ref.stats.naive_fetches
+
+
+@pytest.mark.gpu
+def test_run_cmp_file_streams_matrices(engine, tmp_path):
+    """SMB1 with the flagged full matrices, streamed per block, equals the
+    reference writer's file for the in-memory results."""
+    wl = configs.cmp_small()
+    ds = wl.spec.generate(count=10)
+    p = tmp_path / "c.ssf"
+    write_ssf1(ds, p)
+    cfg = wl.config
+    cfg.kernel_variant = "exact"
+    out = tmp_path / "m.smb"
+    run_cmp_file(engine, p, cfg, smb_path=out, block=4, include_matrix=True)
+    ref = engine.run_cmp(ds, cfg, emit_matrix=True)
+    if oracle.ref_available():
+        b = tmp_path / "ref.smb"
+        oracle.ref_write_picks(b, ref.cdp_id, ref.best_velocity, ref.best_semblance,
+                               ref.values.shape[2], ref.values)
+        assert out.read_bytes() == b.read_bytes()
+    recs = read_smb1(out)
+    np.testing.assert_array_equal(np.stack([r.values for r in recs]), ref.values)
