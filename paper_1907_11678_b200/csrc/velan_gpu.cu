@@ -79,7 +79,7 @@ struct KernelChoice {
 // FAST stage capacities (entries): the default, and the one for traces
 // longer than it holds (one CTA per SM)
 #ifndef VELAN_FAST_CAP
-#define VELAN_FAST_CAP 2560
+#define VELAN_FAST_CAP 5120
 #endif
 constexpr int kFastCap = VELAN_FAST_CAP;
 // large stages: kStages of them in ~190 KB (6016 entries, ns <= 5968, at
@@ -97,7 +97,7 @@ KernelChoice pick() {
   constexpr int CAP = VAR == VAR_FAST ? (CAPF ? CAPF : kFastCap) : 0;
   return KernelChoice{&semblance_scan_kernel<OPK, VAR, WMAX, FIXED, CC, CAP>, CC, CAP,
                       2 * kStages * sizeof(PlanSlot) +
-                          sizeof(float) * kWarps * kBatch * CC * OpTraits<OPK>::NQ};
+                          sizeof(float) * kWarps * kBatch * qs_row(CC, OpTraits<OPK>::NQ)};
 }
 
 template <int OPK, int VAR>
@@ -514,7 +514,7 @@ void set_smem_attr(KernelFn fn, size_t smem) {
                                static_cast<int>(smem)));
 }
 
-// Entries per staging stage: two 256-thread CTAs per SM fit with kStages
+// Entries per staging stage: one 512-thread CTA per SM fits kStages
 // stages.  FAST entries are 16 B (a sample pair and its window energies),
 // EXACT entries fp32 samples.  A stage must hold one whole trace plus the
 // zero pad.
