@@ -402,9 +402,11 @@ struct DeviceState {
     }
     return events[i];
   }
+  int n_sm = 148;
   void init(int d) {
     dev = d;
     VG_CUDA(cudaSetDevice(d));
+    VG_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, d));
     VG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     VG_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
   }
@@ -675,8 +677,9 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
   }
   p.max_legs = max_legs;
   p.max_sweep = max_sweep;
+  // + the consumers' per-tile argmax scratch [2][3][kWarps - 1][kT0]
   const size_t meta_floats = 5 * static_cast<size_t>(max_legs) + max_sweep +
-                             h.n_a + h.n_b + h.n_c;
+                             h.n_a + h.n_b + h.n_c + 6 * (kWarps - 1) * kT0;
   const size_t smem =
       (static_cast<size_t>(kStages) * p.cap * (fast ? 4 : 1) + meta_floats) *
           sizeof(float) +
@@ -723,7 +726,10 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
     }
     const int rb = s.wave_rows[wv], re = s.wave_rows[wv + 1];
     p.row_first = rb;
-    dim3 grid((h.ns + kT0 - 1) / kT0, re - rb);
+    p.n_rows = re - rb;
+    // persistent CTAs, one per SM, striding over the wave's tiles
+    const long long tiles = static_cast<long long>((h.ns + kT0 - 1) / kT0) * (re - rb);
+    dim3 grid(static_cast<unsigned>(std::min<long long>(tiles, D.n_sm)));
     VG_CUDA(cudaEventRecord(D.ev(2 * wv), st));
     kc.fn<<<grid, kThreads, smem, st>>>(p);
     VG_CUDA(cudaGetLastError());
