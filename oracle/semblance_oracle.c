@@ -63,17 +63,22 @@ float vo_traveltime_q(float t0, float h2, float d2, float v) {
   return sqrtf(t0 * t0 + (4.0f * h2 + d2) / (v * v));
 }
 
-/* BASELINE CRS operator, DESIGN.md §3 (no reference implementation):
+/* BASELINE CRS operator, DESIGN.md §3.3 (no reference implementation):
  *   qa = (2*A)*dm ; qb = B*(dm*dm) ; qc = (4*h2)/(v*v)
- *   u  = t0 + qa ; t = sqrt(u*u + ((2*t0)*qb + qc))
- * dm = 0 reduces to vo_traveltime_q(t0, h2, 0, v) bit for bit. */
+ *   (t0 + qa)^2 + 2 t0 qb + qc = t0^2 + 2 t0 beta + gamma with the per
+ *   (trace, candidate) terms beta = qa + qb, gamma = fma(qa, qa, qc):
+ *   t = sqrt(t0*t0 + fma(2*t0, beta, gamma))
+ * (fmaf is correctly rounded, the GPU's FFMA; everything else is compiled
+ * with -ffp-contract=off).  dm = 0 reduces to vo_traveltime_q(t0, h2, 0, v)
+ * bit for bit (beta = 0, gamma = qc). */
 float vo_traveltime_abc(float t0, float h2, float dm, float A, float B,
                         float v) {
   const float qa = (2.0f * A) * dm;
   const float qb = B * (dm * dm);
   const float qc = (4.0f * h2) / (v * v);
-  const float u = t0 + qa;
-  const float t2 = u * u + ((2.0f * t0) * qb + qc);
+  const float beta = qa + qb;
+  const float gamma = fmaf(qa, qa, qc);
+  const float t2 = t0 * t0 + fmaf(2.0f * t0, beta, gamma);
   return sqrtf(t2);
 }
 
