@@ -490,9 +490,14 @@ Shard make_shard(const HostSweep& h, const velan_gpu_dataset* ds, int r0,
       rows_per_wave, std::min<long long>(rows, (148LL * 4 * 8) / per_row_ctas + 1));
   rows_per_wave = std::min<long long>(rows_per_wave, 65535);
   rows_per_wave = std::max<long long>(rows_per_wave, 1);
+  // the first waves ramp up (1/8, 1/4, 1/2 of the target): the upload of
+  // wave 0 is the only one not hidden behind a scan, so keep it small
+  const long long min_rows = std::min<long long>(rows, 148LL * 2 / per_row_ctas + 1);
   int need = 0;
-  for (long long b = 0; b < rows; b += rows_per_wave) {
-    const long long e = std::min(rows, b + rows_per_wave);
+  long long step = rows_per_wave;
+  for (long long b = 0, i = 0; b < rows; b += step, ++i) {
+    step = std::max(min_rows, rows_per_wave >> std::max<long long>(0, 3 - i));
+    const long long e = std::min(rows, b + step);
     for (long long i = s.leg_off[b]; i < s.leg_off[e]; ++i)
       need = std::max(need, s.leg_gather[i] + 1);
     s.wave_rows.push_back(static_cast<int>(b));
