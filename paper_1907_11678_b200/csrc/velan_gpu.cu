@@ -82,8 +82,9 @@ struct KernelChoice {
 #define VELAN_FAST_CAP 5120
 #endif
 constexpr int kFastCap = VELAN_FAST_CAP;
-// large stages: kStages of them in ~190 KB (6016 entries, ns <= 5968, at
-// two stages)
+// large stages: kStages of them in ~190 KB (6080 entries, ns <= 6032, at
+// two stages; an ABC scan with both traces this long and a CRS-large
+// aperture exceeds the 227 KB budget and is refused before any launch)
 constexpr int kFastCapBig = (190 * 1024 / (kStages * 16)) / 32 * 32;
 constexpr int kFastMaxNs = kFastCapBig - 48;  // staging_need(ns) <= cap
 
