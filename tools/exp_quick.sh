@@ -1,6 +1,6 @@
 #!/bin/bash
-# GPU call: default lib vs experimental libs (CMP-large 1024 slice, CRS-small), twice
-O=gpurun_out/exs; mkdir -p $O
+# GPU call: default lib vs the experimental libs under _lib/exp (CMP-large
+# 1024-midpoint slice, CRS-small), twice
 for rep in 1 2; do
 for L in paper_1907_11678_b200/_lib/libvelan_gpu.so $(ls paper_1907_11678_b200/_lib/exp/*.so); do
   n=$(basename $L .so)
