@@ -58,3 +58,40 @@ def reference_synthetic(ncdps, fold, ns, dt_us, events, wavelet_freq=25.0,
                     samples[i, m, s] += np.float32(amp * (1 - 2 * a * a) * math.exp(-a * a))
     return Dataset(samples, coords, np.full(ncdps, fold, np.int32),
                    np.arange(ncdps, dtype=np.uint32), dt_us)
+
+
+def line_dataset(seed, G=10, M=9, ns=240, dt_us=4000, dx=25.0, ragged=True,
+                 poison_padding=True):
+    """A 2-D line of G midpoints dx apart, M half-offsets 50..50M m, U[-1, 1]
+    samples; with ragged=True gather g keeps a random 1..M traces (gather 0
+    keeps M) and the padding slots hold NaN."""
+    rng = np.random.default_rng(seed)
+    samples = rng.uniform(-1.0, 1.0, (G, M, ns)).astype(np.float32)
+    coords = np.zeros((G, M, 4), np.float32)
+    mx = (dx * np.arange(G)).astype(np.float32)
+    h = (50.0 * np.arange(1, M + 1)).astype(np.float32)
+    coords[:, :, 0] = mx[:, None] - h[None, :]   # sx
+    coords[:, :, 2] = mx[:, None] + h[None, :]   # gx
+    ntr = np.full(G, M, np.int32)
+    if ragged:
+        ntr = rng.integers(1, M + 1, G).astype(np.int32)
+        ntr[0] = M
+        ntr[G // 2] = 1
+        for g in range(G):
+            if poison_padding:
+                samples[g, ntr[g]:] = np.nan
+            # the padding's coordinates repeat the first trace's: the
+            # midpoint (types.hpp:57-62) is read from trace 0 only
+            coords[g, ntr[g]:] = coords[g, 0]
+    return Dataset(samples, coords, ntr, np.arange(G, dtype=np.uint32), dt_us)
+
+
+def poison_samples(ds, seed, count):
+    """NaN at `count` seeded (gather, trace, sample) positions inside the
+    gathers' real traces."""
+    rng = np.random.default_rng(seed)
+    for _ in range(count):
+        g = int(rng.integers(0, ds.ncdps))
+        m = int(rng.integers(0, ds.ntraces[g]))
+        ds.samples[g, m, int(rng.integers(0, ds.ns))] = np.nan
+    return ds

@@ -360,3 +360,39 @@ def test_oracle_rejects_invalid_configurations():
         oracle.run_cells(ds, "nmo", 7, np.array([2000.0]), rows, ks)          # ns <= w + 1
     with pytest.raises(ValueError):
         oracle.run_cells(ds, "nmo", 2, np.array([-1.0]), rows, ks)            # v <= 0
+
+
+# ---- ragged gathers and NaN samples (types.hpp:27-39, kernel.hpp:43-50) ----
+@needs_ref
+@pytest.mark.parametrize("poison", [False, True])
+def test_ragged_and_nan_bitwise_vs_reference(poison):
+    """The C restatement on a ragged line (per-gather trace counts 1..M, NaN
+    in the padding slots the reference does not have) and, with poison=True,
+    NaN samples inside real traces: matrix, picks, stacks and valid counts
+    bit for bit against the reference's blocked and baseline kernels, and
+    the d2 CRS sweep against velan::run_crs."""
+    from helpers import line_dataset, poison_samples
+    ds = line_dataset(21)
+    if poison:
+        ds = poison_samples(ds, 6, 10)
+    v = velocity_grid(1500.0, 3500.0, 9)
+    rows, ks = oracle.all_cells(ds.ncdps, ds.ns)
+    a = oracle.run_cells(ds, "nmo", 11, v, rows, ks, matrix=True)
+    for variant in (0, 1):
+        b = oracle.ref_run_cells(ds, "nmo", 11, v, rows, ks, variant=variant, matrix=True, workers=2)
+        np.testing.assert_array_equal(a.matrix.view(np.uint32), b.matrix.view(np.uint32))
+        np.testing.assert_array_equal(a.best_idx, b.best_idx)
+        np.testing.assert_array_equal(np.isnan(a.best_stack), np.isnan(b.best_stack))
+        ok = ~np.isnan(a.best_stack)
+        np.testing.assert_array_equal(a.best_stack[ok].view(np.uint32), b.best_stack[ok].view(np.uint32))
+        assert a.valid == b.valid
+    if poison:
+        assert (a.matrix == 0).any() and np.isnan(a.best_stack).any()
+    code, msg, ref = oracle.ref_run_pipeline(ds, "crs", 1500.0, 3500.0, 9, 11,
+                                             grid=(1, 1), apm=75.0, workers=2)
+    assert code == 0, msg
+    c = oracle.run_cells(ds, "d2", 11, v, rows, ks, apm=75.0, matrix=True)
+    np.testing.assert_array_equal(c.matrix.reshape(ref.matrix.shape).view(np.uint32),
+                                  ref.matrix.view(np.uint32))
+    np.testing.assert_array_equal(c.best_idx.reshape(ref.best_idx.shape), ref.best_idx)
+    assert c.valid == ref.valid
