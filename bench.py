@@ -3,13 +3,17 @@
 search on N B200s, with the FP32 roofline fraction and the host-CPU reference.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload cmp_large|cmp_small|crs_small|crs_large]
+                    [--workload cmp_large|cmp_small|crs_small|crs_large|
+                                scaling_cmp|scaling_crs]
 
 A "step" is one pass of the scan over one rank's workload: the BASELINE
 configuration itself (default configs[1], CMP large: 8192 gathers x 60 traces
 x 2000 samples, 401 candidates, w = 15).  Multi-GPU is weak scaling: every
 rank scans its own contiguous block of a longer line (no collective on the
-data path; only a barrier and the max-over-ranks timing reduction).
+data path; only a barrier and the max-over-ranks timing reduction).  The
+BASELINE scaling sweep (--workload scaling_cmp: 65536 gathers, scaling_crs:
+32768 midpoints) is strong scaling: the fixed line split into contiguous
+blocks (CRS blocks with their replicated +-aperture halo).
 
 One JSON line on rank 0.  ``value`` = nominal evals (midpoints x t0 x
 candidates x traces x w, BASELINE's unit) of all ranks / the max over ranks of
@@ -265,14 +269,25 @@ def main():
     G = wl.spec.n_gathers
     # weak scaling: rank r owns midpoints [r*G, (r+1)*G) of a world*G line;
     # CRS ranks also hold the +-aperture halo (replicated, no exchange) and
-    # restrict their outputs to the owned block (sharding.weak_shard)
-    from paper_1907_11678_b200.sharding import weak_shard
+    # restrict their outputs to the owned block (sharding.weak_shard).
+    # The BASELINE scaling sweep (scaling_cmp / scaling_crs: a fixed 65536-
+    # gather / 32768-midpoint line) is strong scaling: rank r owns the
+    # contiguous block sharding.block_range gives it, plus the halo.
+    from paper_1907_11678_b200.sharding import Shard, block_range, weak_shard
     halo = 0 if wl.op == "nmo" else int(math.ceil(wl.apm / wl.spec.spacing)) + 1
-    shard = weak_shard(G, rank, halo, world)
+    strong = wl.name.startswith("scaling_")
+    if strong:
+        n_line = G
+        b, e = block_range(n_line, world, rank)
+        shard = Shard(rank, (b, e), (max(0, b - halo), min(n_line, e + halo)))
+        G = e - b  # output rows of this rank
+    else:
+        n_line = G * world
+        shard = weak_shard(G, rank, halo, world)
     lo, hi = shard.gathers
     rows = None if wl.op == "nmo" else (shard.row_first, shard.row_count)
     t_gen = time.perf_counter()
-    ds = wl.spec.generate(first=lo, count=hi - lo, n_line=G * world)
+    ds = wl.spec.generate(first=lo, count=hi - lo, n_line=n_line)
     t_gen = time.perf_counter() - t_gen
     w = wl.config.w
 
@@ -396,9 +411,11 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if strong else "weak",
+            "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (seeded generator, BASELINE.json shapes)",
-            "config": {"workload": wl.name, "midpoints_per_gpu": G, "traces": wl.spec.n_traces,
+            "config": {"workload": wl.name, "midpoints_per_gpu": G, "line_midpoints": n_line,
+                       "traces": wl.spec.n_traces,
                        "ns": ns, "dt_us": wl.spec.dt_us, "candidates": wl.ncand, "w": w,
                        "operator": wl.op, "variant": args.variant,
                        "l2": (f"L2 flushed between timed steps (512 MB write; inputs "
