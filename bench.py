@@ -233,7 +233,11 @@ def run_reference_arm(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        # the full step (the workload's nominal evals) at the sampled rate
+        "ms_per_step": wl.nominal_evals() / value * 1e3 if value else None,
+        "ms_per_step_basis": "extrapolated: nominal evals of one full step / sampled rate",
+        "higher_is_better": True,
+        "scaling": "strong" if wl.name.startswith("scaling_") else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": wl.name, "sample": last["sample"]},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads,
