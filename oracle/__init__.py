@@ -23,6 +23,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_LIB = os.path.join(HERE, "libvelan_oracle.so")
+SYNTH_LIB = os.path.join(HERE, "libvelan_synth.so")
 REF_LIB = os.path.join(HERE, "_ref", "libvelan_ref.so")
 
 OP = {"nmo": 0, "d2": 1, "abc": 2}
@@ -30,6 +31,7 @@ _P = C.c_void_p
 
 _oracle = None
 _ref = None
+_synth = None
 
 
 def _p(a):
@@ -61,6 +63,24 @@ def oracle_lib() -> C.CDLL:
     return _oracle
 
 
+def synth_lib() -> C.CDLL:
+    """The seeded input generator (paper_1907_11678_b200/csrc/synth.cpp built
+    without CUDA by oracle/Makefile) for the CPU-only arms: pass it to
+    SynthSpec.generate(lib=...) to make inputs without loading the GPU
+    library."""
+    global _synth
+    if _synth is None:
+        from paper_1907_11678_b200 import _native as N
+        lib = C.CDLL(SYNTH_LIB)
+        for name in ("velan_gpu_synth_generate", "velan_gpu_synth_line_events"):
+            res, args = N.SIGNATURES[name]
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _synth = lib
+    return _synth
+
+
 def ref_available() -> bool:
     return os.path.exists(REF_LIB)
 
@@ -84,6 +104,15 @@ def ref_lib() -> C.CDLL:
             _P, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_uint32, C.c_int,
             C.c_int, C.c_int, _P, C.c_double, C.c_int, C.c_int, _P, _P, C.c_int,
             C.c_int, _P, _P, _P, _P, _P]
+        lib.vref_dataset_create.restype = C.c_void_p
+        lib.vref_dataset_create.argtypes = [_P, _P, _P, _P, C.c_int, C.c_int, C.c_int,
+                                            C.c_uint32]
+        lib.vref_dataset_destroy.restype = None
+        lib.vref_dataset_destroy.argtypes = [_P]
+        lib.vref_run_cells_ds.restype = C.c_int
+        lib.vref_run_cells_ds.argtypes = [
+            _P, C.c_int, C.c_int, C.c_int, _P, C.c_double, C.c_int, C.c_int, _P, _P,
+            C.c_int, C.c_int, _P, _P, _P, _P, _P]
         lib.vref_hit_batch.restype = None
         lib.vref_hit_batch.argtypes = [_P, C.c_int, C.c_double, C.c_int, C.c_int, _P, _P, _P]
         lib.vref_traveltime_batch.restype = None
@@ -131,7 +160,11 @@ def run_cells(ds, op: str, w: int, v, rows, ks, apm: float = 0.0, abc=None,
               mode: int = 0, threads: int = 0, matrix: bool = False,
               stack_matrix: bool = False):
     """The C restatement over output cells (row, k).  mode 0 = kernel
-    arithmetic (scan_pair_baseline order), 1 = oracle.hpp double sums."""
+    arithmetic (scan_pair_baseline order), 1 = oracle.hpp double sums,
+    2 = the blocked trace-outer form (bitwise mode 0, ~25x faster on large
+    sweeps: the checker for the big parity samples and the CPU port
+    baseline), 3 = the literal BASELINE ABC formula in fp64 (the independent
+    pin of the fp32 operator order)."""
     lib = oracle_lib()
     samples, coords, ntr, ids = _flat(ds)
     rows = np.ascontiguousarray(rows, np.int32)
@@ -189,6 +222,57 @@ def ref_run_cells(ds, op: str, w: int, v, rows, ks, apm: float = 0.0,
         OP[op], int(w), len(vv), _p(vv), float(apm), int(variant), int(mode),
         _p(rows), _p(ks), n, int(workers), _p(bi), _p(bs), _p(bst), _p(mat),
         C.addressof(naive))
+    if code != 0:
+        raise RuntimeError(f"reference: code {code}: {lib.vref_last_error().decode()}")
+    return CellResult(bi, bs, bst, mat, int(naive.value))
+
+
+class RefDataset:
+    """A velan::Dataset built once from flat arrays (the reference's own
+    container, types.hpp:14-54), reused across ref_run_cells calls so the
+    per-trace vector copies stay out of timed regions."""
+
+    def __init__(self, ds):
+        samples, coords, ntr, ids = _flat(ds)
+        G, M, ns = samples.shape
+        self.G, self.ns, self.dt_us = G, ns, int(ds.dt_us)
+        self.samples_abs_max = float(np.abs(samples).max()) if samples.size else 0.0
+        self._h = ref_lib().vref_dataset_create(_p(samples), _p(coords), _p(ntr), _p(ids),
+                                                G, M, ns, int(ds.dt_us))
+        if not self._h:
+            raise RuntimeError(ref_lib().vref_last_error().decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            ref_lib().vref_dataset_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def ref_run_cells_ds(rds: RefDataset, op: str, w: int, v, rows, ks, apm: float = 0.0,
+                     variant: int = 1, mode: int = 0, workers: int = 0,
+                     matrix: bool = False):
+    """ref_run_cells on a prebuilt RefDataset."""
+    lib = ref_lib()
+    rows = np.ascontiguousarray(rows, np.int32)
+    ks = np.ascontiguousarray(ks, np.int32)
+    n = len(rows)
+    vv = np.ascontiguousarray(v, np.float32)
+    bi = np.zeros(n, np.int32)
+    bs = np.zeros(n, np.float32)
+    bst = np.zeros(n, np.float32)
+    mat = np.zeros((n, len(vv)), np.float32) if matrix else None
+    naive = C.c_uint64(0)
+    if workers <= 0:
+        workers = os.cpu_count() or 1
+    code = lib.vref_run_cells_ds(rds._h, OP[op], int(w), len(vv), _p(vv), float(apm),
+                                 int(variant), int(mode), _p(rows), _p(ks), n, int(workers),
+                                 _p(bi), _p(bs), _p(bst), _p(mat), C.addressof(naive))
     if code != 0:
         raise RuntimeError(f"reference: code {code}: {lib.vref_last_error().decode()}")
     return CellResult(bi, bs, bst, mat, int(naive.value))

@@ -180,16 +180,35 @@ int vref_run_crs(const float* samples, const float* coords,
 //   variant 0 baseline, 1 blocked (default production), 2 vectorized (L=4)
 //   mode 0 = kernels, 1 = oracle::semblance_reference
 // Rows follow run_cmp (input) / run_crs (cdp_id) order like the GPU ABI.
-int vref_run_cells(const float* samples, const float* coords,
-                   const int32_t* ntraces, const uint32_t* cdp_id, int G,
-                   int M, int ns, uint32_t dt_us, int op, int w, int nc,
-                   const float* v, double apm, int variant, int mode,
-                   const int32_t* cell_row, const int32_t* cell_k,
-                   int n_cells, int workers, int32_t* best_idx, float* best_s,
-                   float* best_stack, float* matrix, uint64_t* naive) {
+// A velan::Dataset built once (the bench's CPU arm keeps the copy out of its
+// timed calls) and reused by vref_run_cells_ds.
+void* vref_dataset_create(const float* samples, const float* coords,
+                          const int32_t* ntraces, const uint32_t* cdp_id, int G,
+                          int M, int ns, uint32_t dt_us) {
   try {
-    const velan::Dataset ds =
-        make_dataset(samples, coords, ntraces, cdp_id, G, M, ns, dt_us);
+    return new velan::Dataset(
+        make_dataset(samples, coords, ntraces, cdp_id, G, M, ns, dt_us));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void vref_dataset_destroy(void* ds) { delete static_cast<velan::Dataset*>(ds); }
+
+int vref_run_cells_ds(const void* dsh, int op, int w, int nc, const float* v,
+                      double apm, int variant, int mode,
+                      const int32_t* cell_row, const int32_t* cell_k,
+                      int n_cells, int workers, int32_t* best_idx,
+                      float* best_s, float* best_stack, float* matrix,
+                      uint64_t* naive) {
+  try {
+    if (!dsh) throw velan::error("null dataset");
+    const velan::Dataset& ds = *static_cast<const velan::Dataset*>(dsh);
+    const int G = static_cast<int>(ds.gathers.size());
+    const int ns = G ? static_cast<int>(ds.gathers[0].ns) : 0;
+    std::vector<uint32_t> cdp_id(G);
+    for (int g = 0; g < G; ++g) cdp_id[g] = ds.gathers[g].cdp_id;
     velan::ScanConfig cfg;
     cfg.w = w;
     cfg.nc = nc;
@@ -204,6 +223,9 @@ int vref_run_cells(const float* samples, const float* coords,
     if (op != 0)
       std::stable_sort(row_gather.begin(), row_gather.end(),
                        [&](int a, int b) { return cdp_id[a] < cdp_id[b]; });
+    for (int c = 0; c < n_cells; ++c)
+      if (cell_row[c] < 0 || cell_row[c] >= G || cell_k[c] < 0 || cell_k[c] >= ns)
+        throw velan::parameter_error("cell outside the dataset");
     std::vector<const velan::CdpGather*> all;
     for (const auto& g : ds.gathers) all.push_back(&g);
 
@@ -212,7 +234,7 @@ int vref_run_cells(const float* samples, const float* coords,
     for (int c = 0; c < n_cells; ++c) by_row[cell_row[c]].push_back(c);
     std::vector<std::pair<int, std::vector<int>>> jobs(by_row.begin(),
                                                        by_row.end());
-    const double dt_s = static_cast<double>(dt_us) * 1e-6;
+    const double dt_s = G ? ds.gathers[0].dt_seconds() : 0.0;
     const int tile = cfg.effective_tile_size();
 
     velan::CacheStats stats;
@@ -313,6 +335,22 @@ int vref_run_cells(const float* samples, const float* coords,
     g_err = e.what();
     return 3;
   }
+}
+
+int vref_run_cells(const float* samples, const float* coords,
+                   const int32_t* ntraces, const uint32_t* cdp_id, int G,
+                   int M, int ns, uint32_t dt_us, int op, int w, int nc,
+                   const float* v, double apm, int variant, int mode,
+                   const int32_t* cell_row, const int32_t* cell_k,
+                   int n_cells, int workers, int32_t* best_idx, float* best_s,
+                   float* best_stack, float* matrix, uint64_t* naive) {
+  void* ds = vref_dataset_create(samples, coords, ntraces, cdp_id, G, M, ns, dt_us);
+  if (!ds) return 3;
+  const int code = vref_run_cells_ds(ds, op, w, nc, v, apm, variant, mode, cell_row,
+                                     cell_k, n_cells, workers, best_idx, best_s,
+                                     best_stack, matrix, naive);
+  vref_dataset_destroy(ds);
+  return code;
 }
 
 // Scalar hooks onto the reference's own inline functions.

@@ -85,9 +85,12 @@ class SynthSpec:
                         "first": first})
 
     def generate(self, first: int = 0, count: Optional[int] = None,
-                 n_threads: int = 0, n_line: Optional[int] = None) -> Dataset:
-        """Gathers [first, first + count) of the full line."""
-        lib = N.load()
+                 n_threads: int = 0, n_line: Optional[int] = None,
+                 lib=None) -> Dataset:
+        """Gathers [first, first + count) of the full line.  ``lib`` may name
+        another build of the same host generator (oracle.synth_lib(): the
+        CPU-only arms generate without loading the GPU library)."""
+        lib = N.load() if lib is None else lib
         count = self.n_gathers if count is None else count
         s = self._struct(first, count, n_threads, n_line)
         samples = np.empty((count, self.n_traces, self.ns), np.float32)

@@ -18,12 +18,21 @@ pytestmark = pytest.mark.gpu
 RTOL = 1e-4
 
 
-def check_cells(gpu_res, ds, wl, rows_gpu, cells_row, cells_k, ref_rows=None, apm=0.0):
+def check_cells(gpu_res, ds, wl, rows_gpu, cells_row, cells_k, ref_rows=None, apm=0.0,
+                kind="port"):
     """Compare GPU picks at sampled cells with the oracle's full candidate
-    sweep of those cells (mode 0 = the reference kernel arithmetic)."""
+    sweep of those cells: kind "port" = the restatement in its blocked form
+    (mode 2, bitwise the reference kernel arithmetic), "ref" = the
+    reference's own blocked kernel (oracle/_ref, NMO / d2 only)."""
     ref_rows = cells_row if ref_rows is None else ref_rows
     ref = oracle.run_cells(ds, wl.op, wl.config.w, wl.config.grid(), ref_rows, cells_k,
-                           apm=apm, abc=wl.abc, matrix=True, stack_matrix=True)
+                           apm=apm, abc=wl.abc, mode=2, matrix=True, stack_matrix=True)
+    if kind == "ref":
+        own = oracle.ref_run_cells(ds, wl.op, wl.config.w, wl.config.grid(), ref_rows,
+                                   cells_k, apm=apm, variant=1, matrix=True)
+        # the restatement's panel is the reference's, bit for bit
+        np.testing.assert_array_equal(own.matrix.view(np.uint32), ref.matrix.view(np.uint32))
+        np.testing.assert_array_equal(own.best_idx, ref.best_idx)
     g_idx = gpu_res.best_idx[rows_gpu, cells_k]
     g_s = gpu_res.best_semblance[rows_gpu, cells_k]
     g_st = gpu_res.stack_trace[rows_gpu, cells_k]
@@ -48,20 +57,25 @@ def sample_cells(rng, n_rows, ns, n):
             rng.integers(0, ns, n).astype(np.int32))
 
 
-def test_cmp_large_full_rows_sampled(engine):
-    """CMP large (8192 x 60 x 2000, 401 C, w 15): 256 gathers on the GPU,
-    1500 seeded cells against the oracle; exact valid count on 4 rows."""
+def test_cmp_large_block_one_percent(engine):
+    """CMP large (8192 x 60 x 2000, 401 C, w 15): a 256-gather block on the
+    GPU; 1 % of its cells (5120: 256 gathers x 20 seeded t0) against the
+    reference's OWN blocked kernel (oracle/_ref scan_tile_blocked, bitwise
+    the restatement's order); exact valid counts on 4 rows."""
     wl = configs.cmp_large()
     wl.config.kernel_variant = "fast"
     ds = wl.spec.generate(first=4000, count=256)
     r = engine.run_cmp(ds, wl.config)
     rng = np.random.default_rng(11)
-    rows, ks = sample_cells(rng, 256, ds.ns, 1500)
-    check_cells(r, ds, wl, rows, rows, ks)
+    rows = np.repeat(np.arange(256, dtype=np.int32), 20)
+    ks = np.concatenate([np.sort(rng.choice(ds.ns, 20, replace=False))
+                         for _ in range(256)]).astype(np.int32)
+    assert len(rows) >= 0.01 * 256 * ds.ns
+    check_cells(r, ds, wl, rows, rows, ks, kind="ref" if oracle.ref_available() else "port")
     sub = ds.subset(range(4))
     r4 = engine.run_cmp(sub, wl.config)
     rr, kk = oracle.all_cells(4, ds.ns)
-    ref = oracle.run_cells(sub, "nmo", 15, wl.config.grid(), rr, kk)
+    ref = oracle.run_cells(sub, "nmo", 15, wl.config.grid(), rr, kk, mode=2)
     assert r4.stats.naive_fetches == ref.valid
     np.testing.assert_array_equal(r4.best_idx, r.best_idx[:4])
 
@@ -79,19 +93,53 @@ def test_crs_small_full(engine):
     check_cells(r, ds, wl, rows, rows, ks, apm=wl.apm)
 
 
-def test_crs_large_block_sampled(engine):
-    """CRS large (4096 x 60 x 2000, +-10 aperture, 21 x 21 x 41, w 15): a
-    32-midpoint block of the line with its halo; 40 seeded cells."""
+def test_crs_large_blocks_sampled(engine):
+    """CRS large (4096 x 60 x 2000, +-10 aperture, 21 x 21 x 41, w 15): three
+    32-midpoint blocks of the line (start, middle, end — truncated apertures
+    included), each with its halo; 1008 seeded cells (21 rows x 16
+    contiguous t0 per block) against the restatement (mode 2)."""
     wl = configs.crs_large()
     wl.config.kernel_variant = "fast"
-    first, count, halo = 2000, 32, 10
-    ds = wl.spec.generate(first=first - halo, count=count + 2 * halo)
-    r = engine.run_crs(ds, wl.config, wl.apm, abc=wl.abc, rows=(halo, count))
-    assert r.best_idx.shape == (count, ds.ns)
-    np.testing.assert_array_equal(r.cdp_id, np.arange(first, first + count))
+    count, halo = 32, 10
     rng = np.random.default_rng(13)
-    rows, ks = sample_cells(rng, count, ds.ns, 40)
-    check_cells(r, ds, wl, rows, rows + halo, ks, apm=wl.apm)
+    total = 0
+    for first in (0, 2000, 4096 - count):
+        lo, hi = max(0, first - halo), min(4096, first + count + halo)
+        ds = wl.spec.generate(first=lo, count=hi - lo)
+        r = engine.run_crs(ds, wl.config, wl.apm, abc=wl.abc, rows=(first - lo, count))
+        assert r.best_idx.shape == (count, ds.ns)
+        np.testing.assert_array_equal(r.cdp_id, np.arange(first, first + count))
+        rows = np.repeat(np.sort(rng.choice(count, 21, replace=False)), 16).astype(np.int32)
+        k0 = rng.integers(0, ds.ns - 16, 21)
+        ks = (np.repeat(k0, 16) + np.tile(np.arange(16), 21)).astype(np.int32)
+        check_cells(r, ds, wl, rows, rows + (first - lo), ks, apm=wl.apm, kind="port")
+        total += len(rows)
+    assert total >= 1000
+
+
+def test_crs_small_fast_vs_literal_fp64_formula(engine):
+    """The ABC operator pinned independently of its fp32 order: the GPU FAST
+    picks on CRS small vs the literal BASELINE formula (t0 + 2A dm)^2 +
+    2 t0 (B dm^2 + C h^2), C = 2/(t0 v^2), in fp64 (oracle mode 3), 400
+    seeded cells x all 2541 candidates: identical picks except near-ties,
+    semblance within 1e-4 relative at the picks."""
+    wl = configs.crs_small()
+    wl.config.kernel_variant = "fast"
+    ds = wl.spec.generate()
+    r = engine.run_crs(ds, wl.config, wl.apm, abc=wl.abc)
+    rng = np.random.default_rng(7)
+    rows, ks = sample_cells(rng, 256, ds.ns, 400)
+    lit = oracle.run_cells(ds, "abc", wl.config.w, None, rows, ks, apm=wl.apm, abc=wl.abc,
+                           mode=3, matrix=True)
+    m = lit.matrix.astype(np.float64)
+    top2 = -np.sort(-m, axis=1)[:, :2]
+    gap = np.abs(top2[:, 0] - top2[:, 1]) / np.maximum(np.abs(top2[:, 0]), 1e-12)
+    g_idx = r.best_idx[rows, ks]
+    same = g_idx == lit.best_idx
+    assert np.all(same | (gap < RTOL)), int((~same & (gap >= RTOL)).sum())
+    at = m[np.arange(len(rows)), g_idx]
+    rel = np.abs(r.best_semblance[rows, ks] - at) / np.maximum(np.abs(at), 1e-12)
+    assert rel.max() <= RTOL, float(rel.max())
 
 
 def test_scaling_shard_equals_slice(engine):
