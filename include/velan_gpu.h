@@ -283,6 +283,16 @@ int velan_ssf1_metadata(const velan_ssf1* f, char* buf, uint64_t cap);
  * buffers to feed asynchronous host->device copies. */
 int velan_ssf1_read(const velan_ssf1* f, int32_t first, int32_t count, int32_t max_traces,
                     float* samples, float* coords, int32_t n_threads);
+/* The same for an arbitrary list of gather indices (a CRS block with its
+ * halo): gathers[i] lands at position i of the layout. */
+int velan_ssf1_read_list(const velan_ssf1* f, const int32_t* gathers, int32_t count,
+                         int32_t max_traces, float* samples, float* coords,
+                         int32_t n_threads);
+/* midpoint_of (types.hpp:57-62) of every gather [n_gathers], from the first
+ * trace's coordinates only (16 bytes per gather read; EPARAM on an empty
+ * gather, as midpoint_of throws) — what a halo-aware block reader needs
+ * before any samples. */
+int velan_ssf1_midpoints(const velan_ssf1* f, float* mx, float* my);
 /* write_dataset (io.hpp:95-122), byte-identical; samples must be host. */
 int velan_ssf1_write(const char* path, const velan_gpu_dataset* ds, const char* metadata,
                      uint64_t metadata_bytes);

@@ -42,6 +42,44 @@ namespace velan_gpu {
 
 enum class Variant { exact = VELAN_VARIANT_EXACT, fast = VELAN_VARIANT_FAST };
 
+// GPU-side options of a drop-in call.  A Variant converts implicitly, so
+// run_cmp(ds, cfg, n, &stats, Variant::fast) keeps working.  values = false
+// leaves SemblanceMatrix::values empty (picks and stack only, as an SMB1 file
+// without matrices, io.hpp:170-194): the full ns x nc matrix is then never
+// allocated, on the device or the host (CMP large: 26 GB).
+struct Options {
+  Variant variant = Variant::exact;
+  bool values = true;
+  Options() = default;
+  Options(Variant v) : variant(v) {}  // NOLINT: implicit on purpose
+  Options(Variant v, bool with_values) : variant(v), values(with_values) {}
+};
+
+// BASELINE's three-parameter CRS search (no reference implementation):
+// candidates A [s/m] x B [s/m^2] x C, the C axis scanned as a velocity
+// (C = 2 / (t0 v^2)); flat index (ia * nB + ib) * nC + ic.
+struct AbcGrid {
+  std::vector<float> a, b, v;
+  int ncand() const { return static_cast<int>(a.size() * b.size() * v.size()); }
+};
+
+// BestPick for the ABC operator: the index triple of the pick (SURVEY.md
+// §8b: BestPick carries one velocity, scan.hpp:81-103).
+struct AbcPick {
+  int32_t ia = 0, ib = 0, ic = 0;
+  float semblance = 0.0f;
+};
+
+// SemblanceMatrix for the ABC operator: values [ns][ncand] sample-major
+// (empty unless requested), the pick triple and the stack at the pick.
+struct AbcMatrix {
+  std::uint32_t cdp_id = 0;
+  int ns = 0, nc = 0;
+  std::vector<float> values;
+  std::vector<AbcPick> best;
+  std::vector<float> stack_trace;
+};
+
 namespace detail {
 
 [[noreturn]] inline void rethrow(int code, const char* where) {
@@ -142,7 +180,7 @@ inline std::vector<const velan::CdpGather*> pointers(const velan::Dataset& ds) {
 inline std::vector<velan::SemblanceMatrix> run(
     std::span<const velan::CdpGather* const> gathers,
     const velan::ScanConfig& cfg, int op, double apm, int devices,
-    Variant variant, velan::CacheStats* stats, int32_t row_first = 0,
+    Options opts, velan::CacheStats* stats, int32_t row_first = 0,
     int32_t row_count = 0) {
   cfg.validate();  // config_error before any compute (scan.hpp:61-78)
   if (gathers.empty()) return {};
@@ -152,7 +190,7 @@ inline std::vector<velan::SemblanceMatrix> run(
   for (int c = 0; c < cfg.nc; ++c) v[c] = grid.value(c);
   velan_gpu_scan sc{};
   sc.op = op;
-  sc.variant = static_cast<int32_t>(variant);
+  sc.variant = static_cast<int32_t>(opts.variant);
   sc.w = cfg.w;
   sc.n_a = sc.n_b = 1;
   sc.n_c = cfg.nc;
@@ -164,13 +202,13 @@ inline std::vector<velan::SemblanceMatrix> run(
   const int rows = row_count > 0 ? row_count : G;
   std::vector<int32_t> best(static_cast<size_t>(rows) * ns), order(rows);
   std::vector<float> sem(best.size()), stk(best.size());
-  std::vector<float> matrix(static_cast<size_t>(rows) * ns * nc);
+  std::vector<float> matrix(opts.values ? static_cast<size_t>(rows) * ns * nc : 0);
   velan_gpu_result res{};
   res.out_mem = VELAN_MEM_HOST;
   res.best_idx = best.data();
   res.best_semblance = sem.data();
   res.best_stack = stk.data();
-  res.matrix = matrix.data();
+  res.matrix = opts.values ? matrix.data() : nullptr;
   res.row_gather = order.data();
   velan_gpu_ctx* ctx = context(devices);
   const int code = op == VELAN_OP_NMO ? velan_gpu_cmp(ctx, &f.ds, &sc, &res)
@@ -183,8 +221,9 @@ inline std::vector<velan::SemblanceMatrix> run(
     m.cdp_id = f.cdp_id[order[r]];
     m.ns = ns;
     m.nc = nc;
-    m.values.assign(matrix.begin() + static_cast<size_t>(r) * ns * nc,
-                    matrix.begin() + static_cast<size_t>(r + 1) * ns * nc);
+    if (opts.values)
+      m.values.assign(matrix.begin() + static_cast<size_t>(r) * ns * nc,
+                      matrix.begin() + static_cast<size_t>(r + 1) * ns * nc);
     m.best_velocity.resize(ns);
     m.stack_trace.resize(ns);
     for (int k = 0; k < ns; ++k) {
@@ -202,11 +241,11 @@ inline std::vector<velan::SemblanceMatrix> run(
 inline std::vector<velan::SemblanceMatrix> run_cmp(
     const velan::Dataset& dataset, const velan::ScanConfig& config,
     int workers, velan::CacheStats* stats_out = nullptr,
-    Variant variant = Variant::exact) {
+    Options options = {}) {
   config.validate();
   if (workers < 1) throw velan::parameter_error("worker count must be >= 1");
   const auto ptrs = detail::pointers(dataset);
-  return detail::run(ptrs, config, VELAN_OP_NMO, 0.0, workers, variant,
+  return detail::run(ptrs, config, VELAN_OP_NMO, 0.0, workers, options,
                      stats_out);
 }
 
@@ -220,7 +259,7 @@ inline std::vector<velan::SemblanceMatrix> run_crs(
     const velan::Dataset& dataset, const velan::ScanConfig& config,
     velan::GridDims dims, double apm, const velan::CrsOptions& options = {},
     velan::CrsRunInfo* info = nullptr, velan::CacheStats* stats_out = nullptr,
-    Variant variant = Variant::exact) {
+    Options opts = {}) {
   config.validate();
   if (options.workers_per_shard < 1)
     throw velan::parameter_error("run_crs: workers_per_shard must be >= 1");
@@ -229,16 +268,16 @@ inline std::vector<velan::SemblanceMatrix> run_crs(
   if (info) info->shards.clear();
   const auto ptrs = detail::pointers(dataset);
   return detail::run(ptrs, config, VELAN_OP_CRS_D2, apm,
-                     options.workers_per_shard, variant, stats_out);
+                     options.workers_per_shard, opts, stats_out);
 }
 
 // scan_cdp (cmp_pipeline.hpp:17-27).
 inline velan::SemblanceMatrix scan_cdp(const velan::CdpGather& gather,
                                        const velan::ScanConfig& config,
-                                       Variant variant = Variant::exact) {
+                                       Options options = {}) {
   const velan::CdpGather* p = &gather;
   auto out = detail::run(std::span<const velan::CdpGather* const>(&p, 1),
-                         config, VELAN_OP_NMO, 0.0, 1, variant, nullptr);
+                         config, VELAN_OP_NMO, 0.0, 1, options, nullptr);
   return std::move(out.front());
 }
 
@@ -247,7 +286,7 @@ inline velan::SemblanceMatrix scan_cdp(const velan::CdpGather& gather,
 inline velan::SemblanceMatrix scan_central_cdp(
     const velan::CdpGather& central,
     std::span<const velan::CdpGather* const> neighbors,
-    const velan::ScanConfig& config, Variant variant = Variant::exact) {
+    const velan::ScanConfig& config, Options options = {}) {
   std::vector<const velan::CdpGather*> all;
   all.push_back(&central);
   double apm = 0.0;
@@ -264,9 +303,72 @@ inline velan::SemblanceMatrix scan_central_cdp(
   int32_t row = 0;
   for (size_t i = 1; i < all.size(); ++i)
     if (all[i]->cdp_id < central.cdp_id) ++row;
-  auto out = detail::run(all, config, VELAN_OP_CRS_D2, apm, 1, variant,
+  auto out = detail::run(all, config, VELAN_OP_CRS_D2, apm, 1, options,
                          nullptr, row, 1);
   return std::move(out.front());
+}
+
+// BASELINE's CRS search with the three-parameter operator
+// t^2 = (t0 + 2 A dm)^2 + 2 t0 (B dm^2 + C h^2) over each midpoint's closed
+// apm ball (neighbors_of, crs_pipeline.hpp:162-180), results in cdp_id order
+// like run_crs.  w is the semblance window (ScanConfig::w); workers = GPUs.
+inline std::vector<AbcMatrix> run_crs_abc(const velan::Dataset& dataset,
+                                          const AbcGrid& grid, int w, double apm,
+                                          int workers = 1,
+                                          velan::CacheStats* stats_out = nullptr,
+                                          Options opts = {}) {
+  if (workers < 1) throw velan::parameter_error("worker count must be >= 1");
+  if (w < 1) throw velan::config_error("ScanConfig: w must be >= 1");
+  if (grid.a.empty() || grid.b.empty() || grid.v.empty())
+    throw velan::config_error("ScanConfig: CRS_ABC needs non-empty A, B and C axes");
+  if (dataset.gathers.empty()) return {};
+  const auto ptrs = detail::pointers(dataset);
+  detail::Flat f = detail::flatten(ptrs);
+  velan_gpu_scan sc{};
+  sc.op = VELAN_OP_CRS_ABC;
+  sc.variant = static_cast<int32_t>(opts.variant);
+  sc.w = w;
+  sc.n_a = static_cast<int32_t>(grid.a.size());
+  sc.n_b = static_cast<int32_t>(grid.b.size());
+  sc.n_c = static_cast<int32_t>(grid.v.size());
+  sc.a = grid.a.data();
+  sc.b = grid.b.data();
+  sc.v = grid.v.data();
+  sc.apm = apm;
+  const int G = f.ds.n_gathers, ns = f.ds.ns, nc = grid.ncand();
+  std::vector<int32_t> best(static_cast<size_t>(G) * ns), order(G);
+  std::vector<float> sem(best.size()), stk(best.size());
+  std::vector<float> matrix(opts.values ? static_cast<size_t>(G) * ns * nc : 0);
+  velan_gpu_result res{};
+  res.out_mem = VELAN_MEM_HOST;
+  res.best_idx = best.data();
+  res.best_semblance = sem.data();
+  res.best_stack = stk.data();
+  res.matrix = opts.values ? matrix.data() : nullptr;
+  res.row_gather = order.data();
+  const int code = velan_gpu_crs(detail::context(workers), &f.ds, &sc, &res);
+  if (code) detail::rethrow(code, "velan_gpu_crs");
+  if (stats_out) stats_out->naive_fetches += res.valid_intersections;
+  const int nB = sc.n_b, nC = sc.n_c;
+  std::vector<AbcMatrix> out(G);
+  for (int r = 0; r < G; ++r) {
+    AbcMatrix& m = out[r];
+    m.cdp_id = f.cdp_id[order[r]];
+    m.ns = ns;
+    m.nc = nc;
+    if (opts.values)
+      m.values.assign(matrix.begin() + static_cast<size_t>(r) * ns * nc,
+                      matrix.begin() + static_cast<size_t>(r + 1) * ns * nc);
+    m.best.resize(ns);
+    m.stack_trace.resize(ns);
+    for (int k = 0; k < ns; ++k) {
+      const size_t o = static_cast<size_t>(r) * ns + k;
+      const int flat = best[o];
+      m.best[k] = AbcPick{flat / (nB * nC), (flat / nC) % nB, flat % nC, sem[o]};
+      m.stack_trace[k] = stk[o];
+    }
+  }
+  return out;
 }
 
 }  // namespace velan_gpu

@@ -35,6 +35,7 @@ from .files import (  # noqa: F401
     read_smb1,
     read_ssf1,
     run_cmp_file,
+    run_crs_file,
     write_smb1,
     write_ssf1,
 )
@@ -45,5 +46,5 @@ __all__ = [
     "VelanError", "describe", "device_count", "neighbors_of", "run_cmp", "run_crs",
     "scan_cdp", "scan_central_cdp", "slowness_grid", "velocity_grid",
     "configs", "FormatError", "SMB1Writer", "SSF1Reader", "read_smb1", "read_ssf1",
-    "run_cmp_file", "write_smb1", "write_ssf1",
+    "run_cmp_file", "run_crs_file", "write_smb1", "write_ssf1",
 ]

@@ -141,6 +141,8 @@ SIGNATURES = {
     "velan_ssf1_gathers": (C.c_int, [_P, _P, _P, _P, _P]),
     "velan_ssf1_metadata": (C.c_int, [_P, _P, C.c_uint64]),
     "velan_ssf1_read": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _P, _P, C.c_int32]),
+    "velan_ssf1_read_list": (C.c_int, [_P, _P, C.c_int32, C.c_int32, _P, _P, C.c_int32]),
+    "velan_ssf1_midpoints": (C.c_int, [_P, _P, _P]),
     "velan_ssf1_write": (C.c_int, [C.c_char_p, C.POINTER(Dataset), C.c_char_p, C.c_uint64]),
     "velan_smb1_begin": (C.c_int, [C.c_char_p, C.c_uint32, C.c_int32, C.c_int32, C.c_int32,
                                    C.POINTER(C.c_void_p)]),

@@ -276,12 +276,14 @@ int velan_ssf1_metadata(const velan_ssf1* f, char* buf, uint64_t cap) {
   IO_END
 }
 
-int velan_ssf1_read(const velan_ssf1* f, int32_t first, int32_t count, int32_t max_traces,
-                    float* samples, float* coords, int32_t n_threads) {
-  IO_BEGIN
-  if (!f || !samples || !coords) throw IoError(VELAN_GPU_EPARAM, "null handle or buffer");
-  if (first < 0 || count < 0 || static_cast<uint64_t>(first) + count > f->cdp_id.size())
-    throw IoError(VELAN_GPU_EPARAM, "gather range outside the file");
+}  // extern "C"
+
+namespace {
+
+// Gathers list[i] (or first + i when list is null), i < count, into the
+// flattened layout: one pread of each gather's whole trace run.
+void read_gathers(const velan_ssf1* f, const int32_t* list, int32_t first, int32_t count,
+                  int32_t max_traces, float* samples, float* coords, int32_t n_threads) {
   if (!f->info.uniform)
     throw IoError(VELAN_GPU_ECONFIG,
                   "gathers differ in ns or dt_us: the flattened layout needs one ns");
@@ -302,7 +304,7 @@ int velan_ssf1_read(const velan_ssf1* f, int32_t first, int32_t count, int32_t m
   auto work = [&]() {
     std::vector<unsigned char> rec;
     for (int i = next++; i < count && !failed; i = next++) {
-      const int g = first + i;
+      const int g = list ? list[i] : first + i;
       const uint32_t M = f->ntraces[g];
       const size_t rb = 16 + 4ull * ns;
       rec.resize(rb * M);
@@ -336,6 +338,54 @@ int velan_ssf1_read(const velan_ssf1* f, int32_t first, int32_t count, int32_t m
   work();
   for (auto& t : th) t.join();
   if (failed) throw IoError(err_code, err);
+}
+
+}  // namespace
+
+extern "C" {
+
+int velan_ssf1_read(const velan_ssf1* f, int32_t first, int32_t count, int32_t max_traces,
+                    float* samples, float* coords, int32_t n_threads) {
+  IO_BEGIN
+  if (!f || !samples || !coords) throw IoError(VELAN_GPU_EPARAM, "null handle or buffer");
+  if (first < 0 || count < 0 || static_cast<uint64_t>(first) + count > f->cdp_id.size())
+    throw IoError(VELAN_GPU_EPARAM, "gather range outside the file");
+  read_gathers(f, nullptr, first, count, max_traces, samples, coords, n_threads);
+  return VELAN_GPU_OK;
+  IO_END
+}
+
+int velan_ssf1_read_list(const velan_ssf1* f, const int32_t* gathers, int32_t count,
+                         int32_t max_traces, float* samples, float* coords,
+                         int32_t n_threads) {
+  IO_BEGIN
+  if (!f || !samples || !coords || (count > 0 && !gathers))
+    throw IoError(VELAN_GPU_EPARAM, "null handle or buffer");
+  if (count < 0) throw IoError(VELAN_GPU_EPARAM, "count < 0");
+  for (int32_t i = 0; i < count; ++i)
+    if (gathers[i] < 0 || static_cast<uint64_t>(gathers[i]) >= f->cdp_id.size())
+      throw IoError(VELAN_GPU_EPARAM, "gather index outside the file");
+  read_gathers(f, gathers, 0, count, max_traces, samples, coords, n_threads);
+  return VELAN_GPU_OK;
+  IO_END
+}
+
+int velan_ssf1_midpoints(const velan_ssf1* f, float* mx, float* my) {
+  IO_BEGIN
+  if (!f || !mx || !my) throw IoError(VELAN_GPU_EPARAM, "null handle or buffer");
+  const size_t G = f->cdp_id.size();
+  unsigned char h[16];
+  for (size_t g = 0; g < G; ++g) {
+    // midpoint_of (types.hpp:57-62): the first trace's source and receiver
+    if (f->ntraces[g] == 0)
+      throw IoError(VELAN_GPU_EPARAM, "midpoint_of: gather " + std::to_string(f->cdp_id[g]) +
+                                          " has no traces");
+    f->file.pread_all(h, 16, f->offset[g]);
+    float c[4];
+    std::memcpy(c, h, 16);  // little-endian host
+    mx[g] = (c[0] + c[2]) * 0.5f;
+    my[g] = (c[1] + c[3]) * 0.5f;
+  }
   return VELAN_GPU_OK;
   IO_END
 }

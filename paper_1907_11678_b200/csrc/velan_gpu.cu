@@ -30,6 +30,7 @@
 #include <exception>
 #include <memory>
 #include <mutex>
+#include <limits>
 #include <numeric>
 #include <stdexcept>
 #include <string>
@@ -63,6 +64,8 @@ struct ApiError : std::runtime_error {
   } while (0)
 
 constexpr int kMaxW = 32;
+// device memory of one per-wave semblance panel (host matrix / top-k scans)
+constexpr size_t kPanelBytes = size_t(4) << 30;
 
 // ---------------------------------------------------------------------------
 // Kernel dispatch: (operator kind, variant, window) -> instantiation.
@@ -392,7 +395,7 @@ enum BufId {
 
 struct DeviceState {
   int dev = 0;
-  cudaStream_t stream = nullptr, copy_stream = nullptr;
+  cudaStream_t stream = nullptr, copy_stream = nullptr, d2h_stream = nullptr;
   DevBuf bufs[B_COUNT];
   std::vector<cudaEvent_t> events;
   cudaEvent_t ev(size_t i) {
@@ -410,6 +413,7 @@ struct DeviceState {
     VG_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, d));
     VG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     VG_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    VG_CUDA(cudaStreamCreateWithFlags(&d2h_stream, cudaStreamNonBlocking));
   }
   void destroy() {
     cudaSetDevice(dev);
@@ -418,7 +422,8 @@ struct DeviceState {
     events.clear();
     if (stream) cudaStreamDestroy(stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
-    stream = copy_stream = nullptr;
+    if (d2h_stream) cudaStreamDestroy(d2h_stream);
+    stream = copy_stream = d2h_stream = nullptr;
   }
 };
 
@@ -432,11 +437,17 @@ struct Shard {
   std::vector<int> ntr;
   std::vector<int> wave_rows;  // wave boundaries (local rows)
   std::vector<int> wave_need;  // local gathers needed up to each wave
+  std::vector<int> wave_lo;    // first local gather a wave's sweeps touch
+  std::vector<int> wave_hi;    // one past the last
+  int max_wave_rows = 0;
+  int table_span = 0;          // max over waves of wave_hi - wave_lo
   long long nominal = 0;
 };
 
+// max_wave_rows caps the rows of one launch (the per-wave semblance panel
+// of a matrix / top-k scan: rows x ns x ncand floats, never a whole shard).
 Shard make_shard(const HostSweep& h, const velan_gpu_dataset* ds, int r0,
-                 int r1, bool identity_gathers) {
+                 int r1, bool identity_gathers, long long max_wave_rows = 65535) {
   Shard s;
   s.r0 = r0;
   s.r1 = r1;
@@ -489,20 +500,30 @@ Shard make_shard(const HostSweep& h, const velan_gpu_dataset* ds, int r0,
       std::max<long long>(1, rows * target_evals / std::max(total_work, 1LL));
   rows_per_wave = std::max<long long>(
       rows_per_wave, std::min<long long>(rows, (148LL * 4 * 8) / per_row_ctas + 1));
-  rows_per_wave = std::min<long long>(rows_per_wave, 65535);
+  const long long cap = std::max<long long>(1, std::min<long long>(max_wave_rows, 65535));
+  rows_per_wave = std::min<long long>(rows_per_wave, cap);
   rows_per_wave = std::max<long long>(rows_per_wave, 1);
   // the first waves ramp up (1/8, 1/4, 1/2 of the target): the upload of
   // wave 0 is the only one not hidden behind a scan, so keep it small
-  const long long min_rows = std::min<long long>(rows, 148LL * 2 / per_row_ctas + 1);
+  const long long min_rows =
+      std::min(cap, std::min<long long>(rows, 148LL * 2 / per_row_ctas + 1));
   int need = 0;
   long long step = rows_per_wave;
   for (long long b = 0, i = 0; b < rows; b += step, ++i) {
     step = std::max(min_rows, rows_per_wave >> std::max<long long>(0, 3 - i));
     const long long e = std::min(rows, b + step);
-    for (long long i = s.leg_off[b]; i < s.leg_off[e]; ++i)
-      need = std::max(need, s.leg_gather[i] + 1);
+    int lo = std::numeric_limits<int>::max(), hi = 0;
+    for (long long i = s.leg_off[b]; i < s.leg_off[e]; ++i) {
+      lo = std::min(lo, s.leg_gather[i]);
+      hi = std::max(hi, s.leg_gather[i] + 1);
+    }
+    need = std::max(need, hi);
     s.wave_rows.push_back(static_cast<int>(b));
     s.wave_need.push_back(need);
+    s.wave_lo.push_back(lo);
+    s.wave_hi.push_back(hi);
+    s.max_wave_rows = std::max<int>(s.max_wave_rows, static_cast<int>(e - b));
+    s.table_span = std::max(s.table_span, hi - lo);
   }
   s.wave_rows.push_back(static_cast<int>(rows));
   return s;
@@ -514,6 +535,30 @@ void upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
   if (!v.empty())
     VG_CUDA(cudaMemcpyAsync(b.p, v.data(), sizeof(T) * v.size(),
                             cudaMemcpyHostToDevice, st));
+}
+
+// Device-resident samples must live on the device that runs the scan: the
+// pointer's owner (cudaPointerGetAttributes) and the declared samples_device
+// both have to match, or the kernels would fault or read a peer over NVLink.
+void check_device_samples(const velan_gpu_dataset* ds, int dev) {
+  if (ds->samples_mem != VELAN_MEM_DEVICE || ds->n_gathers == 0) return;
+  if (ds->samples_device != dev)
+    throw ApiError(VELAN_GPU_ECONFIG,
+                   fmt("device-resident samples declared on device %lld, the context "
+                       "runs on device %lld",
+                       ds->samples_device, dev));
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, ds->samples) != cudaSuccess) {
+    cudaGetLastError();
+    throw ApiError(VELAN_GPU_ECONFIG, "samples_mem is DEVICE but samples is not a CUDA pointer");
+  }
+  if (a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged)
+    throw ApiError(VELAN_GPU_ECONFIG, "samples_mem is DEVICE but samples is host memory");
+  if (a.type == cudaMemoryTypeDevice && a.device != dev)
+    throw ApiError(VELAN_GPU_ECONFIG,
+                   fmt("device-resident samples live on device %lld, the context runs on "
+                       "device %lld",
+                       a.device, dev));
 }
 
 void set_smem_attr(KernelFn fn, size_t smem) {
@@ -551,6 +596,17 @@ struct RunOut {
 // Run one shard on one device.  When out_host is true the result arrays are
 // host memory and rows are copied back at the end; samples are uploaded
 // from host (per wave) unless d_samples_ext is given.
+//
+// Memory is bounded per WAVE (a launch's rows), not per shard:
+//   * FAST tables (16 B per sample) exist only for the gathers the current
+//     wave's sweeps touch [wave_lo, wave_hi) — CRS waves recompute their
+//     halo gathers; the scan kernel indexes the tables relative to
+//     table_trace0;
+//   * a requested semblance panel (host matrix or top-k) is per wave: the
+//     kernel writes rows relative to mat_row0, top-k reduces the wave's panel
+//     in place, and a host matrix leaves the device per wave on its own
+//     stream (two panels alternate so the copy of wave i overlaps the scan
+//     of wave i + 1).
 RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
                  const velan_gpu_dataset* ds, const velan_gpu_scan* sc,
                  velan_gpu_result* res, const float* d_samples_ext,
@@ -578,11 +634,18 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
   }
   const bool out_host = res->out_mem == VELAN_MEM_HOST;
   const size_t cells = static_cast<size_t>(rows) * h.ns;
-  int32_t* d_bidx;
-  float *d_bs, *d_bst, *d_mat = nullptr;
+  const size_t row_cells = static_cast<size_t>(h.ns);
+  const size_t panel_row = row_cells * h.ncand;  // floats per row of a panel
   const int K = res->topk;
+  int32_t* d_bidx;
+  float *d_bs, *d_bst;
   int32_t* d_tki = nullptr;
   float* d_tks = nullptr;
+  // the semblance panel: the caller's device matrix (device-out), or per-wave
+  // internal panels (a host matrix: two alternating; top-k only: one)
+  float* d_mat_user = nullptr;
+  float* d_panel[2] = {nullptr, nullptr};
+  const bool host_matrix = out_host && res->matrix;
   if (out_host) {
     if (K > 0) {
       D.bufs[B_TKI].ensure(cells * K * 4);
@@ -596,25 +659,22 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
     d_bidx = D.bufs[B_BIDX].as<int32_t>();
     d_bs = D.bufs[B_BS].as<float>();
     d_bst = D.bufs[B_BST].as<float>();
-    if (res->matrix) {
-      D.bufs[B_MAT].ensure(cells * h.ncand * 4);
-      d_mat = D.bufs[B_MAT].as<float>();
-    }
   } else {
     d_bidx = res->best_idx + static_cast<size_t>(s.r0) * h.ns;
     d_bs = res->best_semblance + static_cast<size_t>(s.r0) * h.ns;
     d_bst = res->best_stack + static_cast<size_t>(s.r0) * h.ns;
-    if (res->matrix)
-      d_mat = res->matrix + static_cast<size_t>(s.r0) * h.ns * h.ncand;
+    if (res->matrix) d_mat_user = res->matrix + static_cast<size_t>(s.r0) * panel_row;
     if (K > 0) {
       d_tki = res->topk_idx + static_cast<size_t>(s.r0) * h.ns * K;
       d_tks = res->topk_semblance + static_cast<size_t>(s.r0) * h.ns * K;
     }
   }
-  if (K > 0 && !d_mat) {
-    // top-k reads the semblance panel from HBM: an internal matrix buffer
-    D.bufs[B_MAT].ensure(cells * h.ncand * 4);
-    d_mat = D.bufs[B_MAT].as<float>();
+  if (!d_mat_user && (host_matrix || K > 0)) {
+    const size_t panel = static_cast<size_t>(s.max_wave_rows) * panel_row;
+    const int np = host_matrix ? 2 : 1;
+    D.bufs[B_MAT].ensure(panel * np * 4);
+    d_panel[0] = D.bufs[B_MAT].as<float>();
+    d_panel[1] = host_matrix ? d_panel[0] + panel : d_panel[0];
   }
   D.bufs[B_VALID].ensure(8);
   VG_CUDA(cudaMemsetAsync(D.bufs[B_VALID].p, 0, 8, st));
@@ -657,11 +717,15 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
                : (h.ns % 4 == 0) &&
                      (reinterpret_cast<uintptr_t>(d_samples) % 16 == 0);
   p.cap = kc.cap ? kc.cap : staging_cap(h.ns, fast);
+  float2* d_tab = nullptr;
+  size_t tab_traces = 0;
   if (fast) {
-    // pairs then energies, 8 B per sample each
-    D.bufs[B_EC].ensure(std::max<size_t>(1, static_cast<size_t>(L) * trace_floats * 16 + 64));
-    p.pairs = D.bufs[B_EC].as<float2>();
-    p.ec = p.pairs + static_cast<size_t>(L) * trace_floats;
+    // pairs then energies (8 B per sample each) of one wave's gathers
+    tab_traces = static_cast<size_t>(std::max(s.table_span, 1)) * h.M;
+    D.bufs[B_EC].ensure(tab_traces * h.ns * 16 + 64);
+    d_tab = D.bufs[B_EC].as<float2>();
+    p.pairs = d_tab;
+    p.ec = d_tab + tab_traces * h.ns;
   }
   p.dt = h.dt;
   {
@@ -673,7 +737,6 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
   p.best_idx = d_bidx;
   p.best_s = d_bs;
   p.best_stack = d_bst;
-  p.matrix = d_mat;
   p.valid = D.bufs[B_VALID].as<unsigned long long>();
   // per-row metadata staged in shared memory by the kernel
   int max_legs = 1, max_sweep = 1;
@@ -690,15 +753,21 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
       (static_cast<size_t>(kStages) * p.cap * (fast ? 4 : 1) + meta_floats) *
           sizeof(float) +
       kc.slot_bytes;
-  if (smem > 227 * 1024)
+  // the kernel's static __shared__ (barriers, planner state) counts against
+  // the same 227 KB opt-in limit as the dynamic allocation
+  cudaFuncAttributes fa{};
+  VG_CUDA(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(kc.fn)));
+  if (smem + fa.sharedSizeBytes > 227 * 1024)
     throw ApiError(VELAN_GPU_ECONFIG,
                    "scan exceeds the 227 KB shared-memory budget of a CTA "
                    "(too many traces per sweep or candidates)");
   set_smem_attr(kc.fn, smem);
 
   const int nwaves = static_cast<int>(s.wave_need.size());
+  // event slots: [2 wv, 2 wv + 1] timing, [2 nw + wv] upload done,
+  // [3 nw + wv] scan done (panel ready), [4 nw + b] panel b copied out
   int uploaded = 0;
-  int ec_done = 0;
+  int tab_lo = 0, tab_hi = 0;  // gathers the FAST tables currently hold
   for (int wv = 0; wv < nwaves; ++wv) {
     if (upload_samples && s.wave_need[wv] > uploaded) {
       // contiguous runs of global gathers -> one copy each
@@ -718,21 +787,37 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
       VG_CUDA(cudaEventRecord(D.ev(2 * nwaves + wv), D.copy_stream));
       VG_CUDA(cudaStreamWaitEvent(st, D.ev(2 * nwaves + wv), 0));
     }
-    if (fast && s.wave_need[wv] > ec_done) {
-      // window-energy tables of the gathers this wave adds (part of the scan)
-      const long long ntr = static_cast<long long>(s.wave_need[wv] - ec_done) * h.M;
-      const size_t off = static_cast<size_t>(ec_done) * trace_floats;
+    if (fast && !(s.wave_lo[wv] >= tab_lo && s.wave_hi[wv] <= tab_hi)) {
+      // window-energy tables of this wave's gathers (part of the scan)
+      tab_lo = s.wave_lo[wv];
+      tab_hi = s.wave_hi[wv];
+      const long long ntr = static_cast<long long>(tab_hi - tab_lo) * h.M;
       dim3 eg(static_cast<unsigned>(ntr), (h.ns + 255) / 256);
       pair_energy_kernel<<<eg, 256, (256 + h.w + 1) * sizeof(float), st>>>(
-          d_samples + off, const_cast<float2*>(p.pairs) + off,
-          const_cast<float2*>(p.ec) + off, ntr, h.ns, h.w);
+          d_samples + static_cast<size_t>(tab_lo) * trace_floats, d_tab,
+          d_tab + tab_traces * h.ns, ntr, h.ns, h.w);
       VG_CUDA(cudaGetLastError());
-      ec_done = s.wave_need[wv];
+      p.table_trace0 = static_cast<long long>(tab_lo) * h.M;
       ++out.launches;
     }
     const int rb = s.wave_rows[wv], re = s.wave_rows[wv + 1];
     p.row_first = rb;
     p.n_rows = re - rb;
+    float* panel = nullptr;
+    if (d_mat_user) {
+      p.matrix = d_mat_user;
+      p.mat_row0 = 0;
+      panel = d_mat_user + static_cast<size_t>(rb) * panel_row;
+    } else if (d_panel[0]) {
+      panel = d_panel[wv & 1];
+      // the panel's previous contents (wave wv - 2) must have left the device
+      if (host_matrix && wv >= 2) VG_CUDA(cudaStreamWaitEvent(st, D.ev(4 * nwaves + (wv & 1)), 0));
+      p.matrix = panel;
+      p.mat_row0 = rb;
+    } else {
+      p.matrix = nullptr;
+      p.mat_row0 = 0;
+    }
     // persistent CTAs, one per SM, striding over the wave's tiles
     const long long tiles = static_cast<long long>((h.ns + kT0 - 1) / kT0) * (re - rb);
     dim3 grid(static_cast<unsigned>(std::min<long long>(tiles, D.n_sm)));
@@ -741,13 +826,23 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
     VG_CUDA(cudaGetLastError());
     VG_CUDA(cudaEventRecord(D.ev(2 * wv + 1), st));
     ++out.launches;
-  }
-  if (K > 0 && cells > 0) {
-    const long long nc = static_cast<long long>(cells);
-    topk_kernel<<<static_cast<unsigned>((nc + 7) / 8), 256, 0, st>>>(d_mat, nc, h.ncand, K,
-                                                                     d_tks, d_tki);
-    VG_CUDA(cudaGetLastError());
-    ++out.launches;
+    const size_t wcells = static_cast<size_t>(re - rb) * row_cells;
+    if (K > 0) {
+      const long long nc = static_cast<long long>(wcells);
+      topk_kernel<<<static_cast<unsigned>((nc + 7) / 8), 256, 0, st>>>(
+          panel, nc, h.ncand, K, d_tks + static_cast<size_t>(rb) * row_cells * K,
+          d_tki + static_cast<size_t>(rb) * row_cells * K);
+      VG_CUDA(cudaGetLastError());
+      ++out.launches;
+    }
+    if (host_matrix) {
+      VG_CUDA(cudaEventRecord(D.ev(3 * nwaves + wv), st));
+      VG_CUDA(cudaStreamWaitEvent(D.d2h_stream, D.ev(3 * nwaves + wv), 0));
+      VG_CUDA(cudaMemcpyAsync(
+          res->matrix + (static_cast<size_t>(s.r0) + rb) * panel_row, panel,
+          wcells * h.ncand * 4, cudaMemcpyDeviceToHost, D.d2h_stream));
+      VG_CUDA(cudaEventRecord(D.ev(4 * nwaves + (wv & 1)), D.d2h_stream));
+    }
   }
   unsigned long long valid = 0;
   VG_CUDA(cudaMemcpyAsync(&valid, D.bufs[B_VALID].p, 8, cudaMemcpyDeviceToHost,
@@ -759,10 +854,6 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
                             d_bs, cells * 4, cudaMemcpyDeviceToHost, st));
     VG_CUDA(cudaMemcpyAsync(res->best_stack + static_cast<size_t>(s.r0) * h.ns,
                             d_bst, cells * 4, cudaMemcpyDeviceToHost, st));
-    if (res->matrix)
-      VG_CUDA(cudaMemcpyAsync(
-          res->matrix + static_cast<size_t>(s.r0) * h.ns * h.ncand, d_mat,
-          cells * h.ncand * 4, cudaMemcpyDeviceToHost, st));
     if (K > 0) {
       VG_CUDA(cudaMemcpyAsync(res->topk_idx + static_cast<size_t>(s.r0) * h.ns * K, d_tki,
                               cells * K * 4, cudaMemcpyDeviceToHost, st));
@@ -770,6 +861,7 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
                               d_tks, cells * K * 4, cudaMemcpyDeviceToHost, st));
     }
   }
+  if (host_matrix) VG_CUDA(cudaStreamSynchronize(D.d2h_stream));
   VG_CUDA(cudaStreamSynchronize(st));
   out.valid = valid;
   for (int wv = 0; wv < nwaves; ++wv) {
@@ -974,6 +1066,7 @@ static int run_oneshot(velan_gpu_ctx* ctx, const velan_gpu_dataset* ds,
   if (res->out_mem == VELAN_MEM_DEVICE && ctx->devs.size() != 1)
     throw ApiError(VELAN_GPU_ECONFIG,
                    "device-resident outputs need a single-device context");
+  check_device_samples(ds, ctx->devs[0].dev);
   std::lock_guard<std::mutex> guard(ctx->lock);
   const HostSweep h = build_sweep(ds, sc);
   const int nd = static_cast<int>(ctx->devs.size());
@@ -982,9 +1075,17 @@ static int run_oneshot(velan_gpu_ctx* ctx, const velan_gpu_dataset* ds,
   std::vector<std::string> errs(nd);
   std::vector<int> codes(nd, 0);
   const bool dev_samples = ds->samples_mem == VELAN_MEM_DEVICE;
+  // a semblance panel that is not the caller's device matrix is per wave:
+  // cap a wave's rows so one panel stays within kPanelBytes
+  long long wave_cap = 65535;
+  const bool internal_panel =
+      res->topk > 0 || (res->matrix && res->out_mem == VELAN_MEM_HOST);
+  if (internal_panel)
+    wave_cap = std::max<long long>(
+        1, static_cast<long long>(kPanelBytes / (static_cast<size_t>(h.ns) * h.ncand * 4)));
   auto body = [&](int i) {
     try {
-      const Shard s = make_shard(h, ds, cuts[i], cuts[i + 1], dev_samples);
+      const Shard s = make_shard(h, ds, cuts[i], cuts[i + 1], dev_samples, wave_cap);
       outs[i] = run_shard(ctx->devs[i], h, s, ds, sc, res,
                           dev_samples ? ds->samples : nullptr, nullptr, false,
                           false);
@@ -1044,6 +1145,7 @@ int velan_gpu_plan_create(velan_gpu_ctx* ctx, const velan_gpu_dataset* ds,
   validate(ds, sc, sc && sc->op != VELAN_OP_NMO);
   if (ctx->devs.size() != 1)
     throw ApiError(VELAN_GPU_ECONFIG, "plans need a single-device context");
+  check_device_samples(ds, ctx->devs[0].dev);
   auto plan = std::make_unique<velan_gpu_plan>();
   plan->ctx = ctx;
   plan->ds = *ds;

@@ -314,3 +314,148 @@ def run_cmp_file(engine: Engine, ssf_path: str, config: ScanConfig,
                 N.load().velan_smb1_end(writer._h)
                 writer._h = None
     return results if keep_results else {"valid_intersections": valid, "kernel_ms": kernel_ms}
+
+
+# --------------------------------------------------------------------------
+# streaming file -> GPU -> file pipeline (CRS, halo-aware blocks)
+
+def check_partition(mx: np.ndarray, my: np.ndarray, dims: tuple, apm: float) -> None:
+    """partition()'s configuration checks (crs_pipeline.hpp:92-158), which
+    run_crs applies before any compute: grid dims >= 1, apm > 0, finite
+    midpoints, and apm at most half a shard's width / height.  The results
+    do not depend on the grid (run_crs matches a 1 x 1 grid run); the GPU
+    path blocks the line its own way."""
+    gx, gy = dims
+    if gx < 1 or gy < 1:
+        raise ConfigError("partition: grid dims must be >= 1")
+    if not apm > 0.0:
+        raise ConfigError("partition: apm must be > 0")
+    if len(mx) == 0:
+        raise ParameterError("partition: dataset has no CDPs")
+    if not (np.isfinite(mx).all() and np.isfinite(my).all()):
+        raise ParameterError("partition: non-finite midpoint")
+    w = (float(mx.max()) - float(mx.min())) / (gx if gx > 1 else 1)
+    h = (float(my.max()) - float(my.min())) / (gy if gy > 1 else 1)
+    if gx > 1 and apm > w / 2.0:
+        raise ConfigError(f"partition: apm {apm} exceeds half the shard width {w / 2.0}")
+    if gy > 1 and apm > h / 2.0:
+        raise ConfigError(f"partition: apm {apm} exceeds half the shard height {h / 2.0}")
+
+
+def crs_blocks(mx: np.ndarray, my: np.ndarray, cdp_id: np.ndarray, apm: float,
+               block: int) -> list:
+    """Halo-aware blocks of a CRS line / grid: the output rows in cdp_id order
+    (ties by file index, run_crs's order, crs_pipeline.hpp:449-459) cut into
+    runs of ``block`` rows; each block lists the file gathers it needs — its
+    own rows plus every gather within the closed apm ball of one of them
+    (neighbors_of, crs_pipeline.hpp:162-180: double test of the fp32
+    difference) — in file order, and the position of its first own row in
+    that subset's cdp_id order.  Returns [(rows, gathers, row_first)]."""
+    G = len(cdp_id)
+    order = np.lexsort((np.arange(G), cdp_id.astype(np.int64)))
+    by_x = np.argsort(mx, kind="stable")
+    xs = mx[by_x].astype(np.float64)
+    margin = apm * 1e-5 + 1e-3
+    out = []
+    for s in range(0, G, block):
+        rows = order[s:s + block]
+        need = set(int(g) for g in rows)
+        for g in rows:
+            lo = np.searchsorted(xs, float(mx[g]) - apm - margin, "left")
+            hi = np.searchsorted(xs, float(mx[g]) + apm + margin, "right")
+            cand = by_x[lo:hi]
+            dx = (mx[cand] - mx[g]).astype(np.float32).astype(np.float64)
+            dy = (my[cand] - my[g]).astype(np.float32).astype(np.float64)
+            for o in cand[dx * dx + dy * dy <= apm * apm]:
+                need.add(int(o))
+        gathers = np.array(sorted(need), np.int32)
+        # own rows are contiguous in the subset's (cdp_id, index) order
+        key = lambda g: (int(cdp_id[g]), int(g))  # noqa: E731
+        first_key = key(int(rows[0]))
+        row_first = sum(1 for g in gathers if key(int(g)) < first_key)
+        out.append((rows, gathers, row_first))
+    return out
+
+
+def run_crs_file(engine: Engine, ssf_path: str, config: ScanConfig, apm: float,
+                 smb_path: Optional[str] = None, dims: tuple = (1, 1), abc=None,
+                 block: int = 256, threads: int = 0, keep_results: bool = True,
+                 include_matrix: bool = False):
+    """``velan crs --data F --out P --grid GXxGY --apm A [--matrix]``
+    (tools/velan.cpp:167-184: read_dataset, run_crs, write_picks) as a
+    stream: the SSF1 file is indexed (headers and first-trace coordinates
+    only), the cdp_id-ordered output rows are cut into blocks, and each
+    block's gathers plus its +-apm halo are read (one pread per gather, a
+    reader thread filling the next pinned block while the GPU scans the
+    current one) and scanned with the outputs restricted to the block.  The
+    SMB1 records are appended block by block in run_crs's order, so the file
+    is byte-identical to velan::run_crs + write_picks (EXACT variant).
+    ``abc`` selects BASELINE's three-parameter operator (SMB1's velocity
+    column then holds the C-axis velocity of the pick)."""
+    config.validate()
+    lib = N.load()
+    with SSF1Reader(ssf_path) as rd:
+        if not rd.uniform:
+            raise ConfigError("run_crs_file: gathers differ in ns or dt_us")
+        G = rd.n_gathers
+        if G == 0:
+            if smb_path:
+                with SMB1Writer(smb_path, 0, 0, 0, include_matrix):
+                    pass
+            return [] if keep_results else {"valid_intersections": 0, "kernel_ms": 0.0}
+        mx = np.zeros(G, np.float32)
+        my = np.zeros(G, np.float32)
+        _check(lib.velan_ssf1_midpoints(rd._h, _ptr(mx), _ptr(my)), "velan_ssf1_midpoints")
+        check_partition(mx, my, dims, apm)
+        blocks = crs_blocks(mx, my, rd.cdp_id, apm, block)
+        cap = max(len(b[1]) for b in blocks)
+        bufs = [(_alloc((cap, rd.fold, rd.ns), np.float32, True),
+                 _alloc((cap, rd.fold, 4), np.float32, True)) for _ in range(2)]
+        ncand = abc.ncand if abc is not None else len(config.grid())
+        writer = SMB1Writer(smb_path, G, rd.ns, ncand, include_matrix) if smb_path else None
+        results, valid, kernel_ms = [], 0, 0.0
+        pending, err = {}, []
+
+        def load(i):
+            try:
+                gl = blocks[i][1]
+                sm, co = bufs[i % 2]
+                _check(lib.velan_ssf1_read_list(rd._h, _ptr(gl), len(gl), rd.fold, _ptr(sm),
+                                                _ptr(co), threads), "velan_ssf1_read_list")
+                n = len(gl)
+                pending[i] = Dataset(sm[:n], co[:n], rd.ntraces[gl].copy(),
+                                     rd.cdp_id[gl].copy(), rd.dt_us)
+            except BaseException as e:  # surfaced in the main thread
+                err.append(e)
+
+        th = threading.Thread(target=load, args=(0,))
+        th.start()
+        try:
+            for i, (rows, gl, row_first) in enumerate(blocks):
+                th.join()
+                if err:
+                    raise err[0]
+                ds = pending.pop(i)
+                if i + 1 < len(blocks):
+                    th = threading.Thread(target=load, args=(i + 1,))
+                    th.start()
+                r = engine.run_crs(ds, config, apm, abc, emit_matrix=include_matrix,
+                                   rows=(row_first, len(rows)))
+                r.row_gather = gl[r.row_gather]  # file gather of every row
+                valid += r.stats.naive_fetches
+                kernel_ms += r.kernel_ms
+                if writer is not None:
+                    writer.append_result(r)
+                if keep_results:
+                    if include_matrix and smb_path:
+                        r.values = None
+                    results.append(r)
+            if writer is not None:
+                writer.close()
+        finally:
+            if th.is_alive():
+                th.join()
+            if writer is not None and getattr(writer, "_h", None):
+                lib.velan_smb1_end(writer._h)
+                writer._h = None
+    return results if keep_results else {"valid_intersections": valid, "kernel_ms": kernel_ms}

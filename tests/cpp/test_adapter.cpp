@@ -4,6 +4,8 @@
 // Built by oracle/Makefile against the UNMODIFIED reference headers into
 // oracle/_ref/test_adapter (test infrastructure; needs a B200 to run).  Exit
 // code = number of failed checks.
+#include <sys/resource.h>
+
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -62,7 +64,53 @@ velan::Dataset synthetic(int ncdps, double snr, double spacing = 25.0,
 
 }  // namespace
 
-int main() {
+// CMP large through the drop-in with values = false: 8192 gathers x 60 x
+// 2000 samples (the reference's own containers, 3.9 GB), picks only.  Peak
+// RSS stays far below the 26 GB the full matrix would take.
+int large_picks_only() {
+  velan::Dataset ds;
+  ds.fold = 60;
+  ds.gathers.resize(8192);
+  std::mt19937 rng(5);
+  std::uniform_real_distribution<float> u(-1.0f, 1.0f);
+  std::vector<float> noise(1 << 16);
+  for (float& x : noise) x = u(rng);
+  for (int g = 0; g < 8192; ++g) {
+    velan::CdpGather& cg = ds.gathers[g];
+    cg.cdp_id = g;
+    cg.ns = 2000;
+    cg.dt_us = 2000;
+    cg.traces.resize(60);
+    for (int m = 0; m < 60; ++m) {
+      velan::Trace& t = cg.traces[m];
+      const float h = 25.0f * (m + 1), mx = 25.0f * g;
+      t.sx = mx - h;
+      t.gx = mx + h;
+      t.samples.resize(2000);
+      const size_t off = (static_cast<size_t>(g) * 60 + m) * 2000 % (noise.size() - 2000);
+      std::memcpy(t.samples.data(), noise.data() + off, 2000 * 4);
+    }
+  }
+  velan::ScanConfig cfg;
+  cfg.nc = 401;
+  cfg.w = 15;
+  cfg.vmin = 1400.0f;
+  cfg.vmax = 5000.0f;
+  velan::CacheStats st;
+  const auto out = velan_gpu::run_cmp(ds, cfg, 1, &st,
+                                      velan_gpu::Options{velan_gpu::Variant::fast, false});
+  struct rusage ru;
+  getrusage(RUSAGE_SELF, &ru);
+  const double rss_gb = ru.ru_maxrss / 1048576.0;
+  check(out.size() == 8192 && out[0].values.empty() && out[8191].best_velocity.size() == 2000,
+        "CMP large, values = false: 8192 picked gathers");
+  check(rss_gb < 16.0, "peak RSS without the 26 GB matrix", std::to_string(rss_gb) + " GB");
+  std::printf("%d failure(s)\n", failures);
+  return failures;
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "large") return large_picks_only();
   // 1. run_cmp: bitwise equal to the reference pipeline (blocked kernel)
   {
     const velan::Dataset ds = synthetic(6, 3.0);
@@ -158,6 +206,61 @@ int main() {
     const auto rep = velan::oracle::compare(gpu, ref);
     check(max_rel <= 1e-4 && rep.argmax_mismatches == 0, "FAST variant within 1e-4",
           "max_rel=" + std::to_string(max_rel));
+  }
+  // 7. values = false: the same picks and stack, no matrix anywhere
+  {
+    const velan::Dataset ds = synthetic(5, 5.0);
+    velan::ScanConfig cfg;
+    cfg.nc = 33;
+    cfg.w = 4;
+    const auto full = velan_gpu::run_cmp(ds, cfg, 1);
+    velan::CacheStats st;
+    const auto picks = velan_gpu::run_cmp(ds, cfg, 1, &st, velan_gpu::Options{velan_gpu::Variant::exact, false});
+    bool ok = picks.size() == full.size();
+    for (size_t i = 0; ok && i < full.size(); ++i) {
+      ok = picks[i].values.empty() && picks[i].cdp_id == full[i].cdp_id &&
+           same_bits(picks[i].stack_trace, full[i].stack_trace);
+      for (int k = 0; ok && k < full[i].ns; ++k)
+        ok = std::memcmp(&picks[i].best_velocity[k], &full[i].best_velocity[k],
+                         sizeof(velan::BestPick)) == 0;
+    }
+    check(ok && st.naive_fetches > 0, "values = false: picks and stack only");
+  }
+  // 8. run_crs_abc: with the aperture holding only the central gather
+  //    (dm = 0) the three-parameter operator is NMO bit for bit, so the
+  //    picks equal velan::run_cmp's (ia = ib = 0 by the tie rule) and every
+  //    (A, B) column of the matrix equals the reference's v column
+  {
+    const velan::Dataset ds = synthetic(4, 5.0, 200.0);
+    velan::ScanConfig cfg;
+    cfg.nc = 17;
+    cfg.w = 5;
+    const auto ref = velan::run_cmp(ds, cfg, 1);
+    velan_gpu::AbcGrid grid;
+    grid.a = {-2e-4f, 0.0f, 1e-4f};
+    grid.b = {0.0f, 5e-8f};
+    for (int c = 0; c < cfg.nc; ++c) grid.v.push_back(cfg.grid().value(c));
+    velan::CacheStats st;
+    const auto abc = velan_gpu::run_crs_abc(ds, grid, cfg.w, 1.0, 1, &st);
+    bool ok = abc.size() == ref.size();
+    const int nab = 6, nc = cfg.nc;
+    for (size_t i = 0; ok && i < ref.size(); ++i) {
+      ok = abc[i].cdp_id == ref[i].cdp_id && same_bits(abc[i].stack_trace, ref[i].stack_trace) &&
+           abc[i].nc == nab * nc;
+      for (int k = 0; ok && k < ref[i].ns; ++k) {
+        const velan_gpu::AbcPick& p = abc[i].best[k];
+        ok = p.ia == 0 && p.ib == 0 && grid.v[p.ic] == ref[i].best_velocity[k].velocity &&
+             std::memcmp(&p.semblance, &ref[i].best_velocity[k].semblance, 4) == 0;
+        for (int ab = 0; ok && ab < nab; ++ab)
+          for (int c = 0; ok && c < nc; ++c)
+            ok = std::memcmp(&abc[i].values[static_cast<size_t>(k) * nab * nc + ab * nc + c],
+                             &ref[i].values[static_cast<size_t>(k) * nc + c], 4) == 0;
+      }
+    }
+    check(ok && st.naive_fetches > 0, "run_crs_abc (dm = 0) == run_cmp bitwise, (ia, ib, ic) picks");
+    bool cfg_err = false;
+    try { velan_gpu::run_crs_abc(ds, velan_gpu::AbcGrid{}, 5, 1.0); } catch (const velan::config_error&) { cfg_err = true; }
+    check(cfg_err, "run_crs_abc: empty axes -> config_error");
   }
   std::printf("%d failure(s)\n", failures);
   return failures;

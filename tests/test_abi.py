@@ -136,3 +136,42 @@ def test_python_config_validation():
         ScanConfig(vmin=0.0).validate()
     with pytest.raises(ConfigError):
         ScanConfig(kernel_variant="simd").validate()
+
+
+@pytest.mark.gpu
+def test_device_samples_must_live_on_the_context_device():
+    """samples_mem = DEVICE with a host pointer, or declared on another
+    device, is a config error before any launch (no fault, no peer read)."""
+    import torch
+    from paper_1907_11678_b200 import ConfigError, Dataset, Engine, ScanConfig, configs
+    wl = configs.cmp_small()
+    ds = wl.spec.generate(count=2)
+    eng = Engine([0])
+    cfg = ScanConfig(w=11, velocities=wl.config.grid(), kernel_variant="fast")
+    dev = torch.from_numpy(ds.samples).cuda()
+    dd = Dataset(dev, ds.coords, ds.ntraces, ds.cdp_id, ds.dt_us)
+    eng.run_cmp(dd, cfg)  # fine
+    from paper_1907_11678_b200 import api
+    orig = api._dataset_struct
+
+    def lie_device(d):
+        s = orig(d)
+        s.samples_device = 5
+        return s
+
+    def lie_host(d):
+        s = orig(d)
+        s.samples_mem = 1  # MEM_DEVICE
+        return s
+    try:
+        api._dataset_struct = lie_device
+        with pytest.raises(ConfigError):
+            eng.run_cmp(dd, cfg)
+        with pytest.raises(ConfigError):
+            eng.plan(dd, cfg)
+        api._dataset_struct = lie_host
+        with pytest.raises(ConfigError):
+            eng.run_cmp(ds, cfg)
+    finally:
+        api._dataset_struct = orig
+        eng.close()

@@ -238,3 +238,115 @@ def test_run_cmp_file_streams_matrices(engine, tmp_path):
         assert out.read_bytes() == b.read_bytes()
     recs = read_smb1(out)
     np.testing.assert_array_equal(np.stack([r.values for r in recs]), ref.values)
+
+
+# ---------------------------------------------------------------- CRS file pipeline
+
+def grid_dataset(nx=6, ny=5, M=6, ns=160, dt_us=2000, seed=8, shuffle=True):
+    """A 2-D grid of midpoints 25 m apart, cdp_id row-major, written to the
+    file in a shuffled order (run_crs orders its output by cdp_id)."""
+    rng = np.random.default_rng(seed)
+    G = nx * ny
+    samples = rng.uniform(-1, 1, (G, M, ns)).astype(np.float32)
+    coords = np.zeros((G, M, 4), np.float32)
+    ids = np.arange(G, dtype=np.uint32)
+    h = (40.0 * np.arange(1, M + 1)).astype(np.float32)
+    for g in range(G):
+        mx, my = np.float32(25.0 * (g % nx)), np.float32(25.0 * (g // nx))
+        coords[g, :, 0] = mx - h
+        coords[g, :, 2] = mx + h
+        coords[g, :, 1] = coords[g, :, 3] = my
+    perm = rng.permutation(G) if shuffle else np.arange(G)
+    return Dataset(samples[perm], coords[perm], np.full(G, M, np.int32), ids[perm], dt_us)
+
+
+def test_ssf1_midpoints_and_gather_lists(tmp_path):
+    ds = grid_dataset()
+    p = tmp_path / "g.ssf"
+    write_ssf1(ds, p)
+    from paper_1907_11678_b200 import _native as N
+    from paper_1907_11678_b200.api import _ptr
+    with SSF1Reader(p) as rd:
+        mx = np.zeros(rd.n_gathers, np.float32)
+        my = np.zeros(rd.n_gathers, np.float32)
+        assert N.load().velan_ssf1_midpoints(rd._h, _ptr(mx), _ptr(my)) == 0
+        np.testing.assert_array_equal(np.stack([mx, my], 1), ds.midpoints())
+        gl = np.array([7, 2, 29, 2], np.int32)
+        sm = np.zeros((4, rd.fold, rd.ns), np.float32)
+        co = np.zeros((4, rd.fold, 4), np.float32)
+        assert N.load().velan_ssf1_read_list(rd._h, _ptr(gl), 4, rd.fold, _ptr(sm),
+                                             _ptr(co), 2) == 0
+        np.testing.assert_array_equal(sm, ds.samples[gl])
+        np.testing.assert_array_equal(co, ds.coords[gl])
+
+
+def test_crs_blocks_hold_every_sweep():
+    """Each block's gather list contains the full sweep (central + closed apm
+    ball, the library's own sweep builder) of every row it owns, and the
+    blocks tile the cdp_id-ordered rows."""
+    from paper_1907_11678_b200 import describe
+    from paper_1907_11678_b200.files import crs_blocks
+    ds = grid_dataset()
+    cfg = ScanConfig(w=5, nc=7)
+    apm = 36.0  # the 8-neighbourhood on a 25 m grid
+    sw = describe(ds, cfg, op="d2", apm=apm)
+    mp = ds.midpoints()
+    blocks = crs_blocks(mp[:, 0], mp[:, 1], ds.cdp_id, apm, 7)
+    allrows = np.concatenate([b[0] for b in blocks])
+    np.testing.assert_array_equal(allrows, sw.row_gather)
+    for rows, gathers, row_first in blocks:
+        for g in rows:
+            r = int(np.nonzero(sw.row_gather == g)[0][0])
+            legs = sw.leg_gather[sw.leg_off[r]:sw.leg_off[r + 1]]
+            assert set(legs.tolist()) <= set(gathers.tolist())
+        sub = describe(ds.subset(gathers), cfg, op="d2", apm=apm)
+        np.testing.assert_array_equal(gathers[sub.row_gather[row_first:row_first + len(rows)]],
+                                      rows)
+
+
+def test_crs_partition_checks_match_reference():
+    from paper_1907_11678_b200.files import check_partition
+    ds = grid_dataset(shuffle=False)
+    mp = ds.midpoints()
+    check_partition(mp[:, 0], mp[:, 1], (2, 1), 30.0)
+    check_partition(mp[:, 0], mp[:, 1], (1, 1), 300.0)
+    with pytest.raises(ConfigError):   # 125 m / 2 shards -> half width 31.25
+        check_partition(mp[:, 0], mp[:, 1], (2, 1), 31.5)
+    with pytest.raises(ConfigError):   # 100 m / 2 shards -> half height 25
+        check_partition(mp[:, 0], mp[:, 1], (2, 2), 30.0)
+    with pytest.raises(ConfigError):
+        check_partition(mp[:, 0], mp[:, 1], (1, 1), 0.0)
+    with pytest.raises(ConfigError):
+        check_partition(mp[:, 0], mp[:, 1], (0, 1), 5.0)
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("with_matrix", [False, True])
+def test_run_crs_file_byte_identical_to_reference(engine, tmp_path, with_matrix):
+    """velan crs --data F --out P --grid 2x1 --apm 30 [--matrix]
+    (tools/velan.cpp:167-184 = read_dataset + velan::run_crs + write_picks,
+    all from oracle/_ref) against run_crs_file streaming the same SSF1 file in
+    halo-aware blocks through the GPU (EXACT): the pick files are
+    byte-identical."""
+    from paper_1907_11678_b200 import run_crs_file
+    ds = grid_dataset()
+    p = tmp_path / "g.ssf"
+    write_ssf1(ds, p)
+    cfg = ScanConfig(vmin=1500.0, vmax=3500.0, nc=9, w=5, kernel_variant="exact")
+    code, msg, ref = oracle.ref_run_pipeline(ds, "crs", 1500.0, 3500.0, 9, 5, workers=2,
+                                             grid=(2, 1), apm=30.0, matrix=True)
+    assert code == 0, msg
+    order = np.lexsort((np.arange(ds.ncdps), ds.cdp_id))
+    v = cfg.grid()
+    refp = tmp_path / "ref.smb"
+    oracle.ref_write_picks(refp, ds.cdp_id[order], v[ref.best_idx], ref.best_semblance, 9,
+                           ref.matrix if with_matrix else None)
+    out = tmp_path / "gpu.smb"
+    blocks = run_crs_file(engine, p, cfg, 30.0, smb_path=out, dims=(2, 1), block=7,
+                          include_matrix=with_matrix)
+    assert len(blocks) == 5
+    assert out.read_bytes() == refp.read_bytes()
+    assert sum(b.stats.naive_fetches for b in blocks) == ref.valid
+    with pytest.raises(ConfigError):
+        run_crs_file(engine, p, cfg, 40.0, dims=(2, 1))

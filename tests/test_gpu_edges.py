@@ -105,3 +105,42 @@ def test_nan_samples(engine, variant):
     ref = oracle.run_cells(ds, "nmo", 15, v, rows, ks, matrix=True)
     assert np.isnan(ref.best_stack).any() or (ref.matrix == 0).any()
     check(r, ref, ds.ns, len(v), variant, 9)
+
+
+def _canon(a):
+    a = np.array(a, np.float32)
+    a[np.isnan(a)] = np.float32("nan")
+    return a.view(np.uint32)
+
+
+def test_inf_samples_nan_semblance_pick_rule(engine):
+    """+Inf samples make den = inf and sum_sq = inf, so the reference's
+    semblance is inf/inf = NaN (kernel.hpp:43-50).  scan_sweep's pick
+    (scan.hpp:167-179: best = S[0], strict '>') then keeps candidate 0 when
+    S[0] is NaN, and never picks a NaN elsewhere.  The kernel's argmax runs in
+    any order across warps and must follow the same rule: EXACT bitwise
+    (NaNs canonicalised), picks identical, on cells of both kinds; top-k's
+    entry 0 is the pick."""
+    ds = line_dataset(14, ragged=False)
+    rng = np.random.default_rng(21)
+    for _ in range(40):
+        g, m, k = int(rng.integers(0, ds.ncdps)), int(rng.integers(0, 9)), int(rng.integers(20, 230))
+        ds.samples[g, m, k] = np.inf
+    v = velocity_grid(1500.0, 3500.0, 37)
+    cfg = ScanConfig(w=11, velocities=v, kernel_variant="exact")
+    r = engine.run_cmp(ds, cfg, emit_matrix=True, topk=3)
+    rows, ks = oracle.all_cells(ds.ncdps, ds.ns)
+    ref = oracle.run_cells(ds, "nmo", 11, v, rows, ks, matrix=True)
+    nan0 = np.isnan(ref.matrix[:, 0])
+    nan_other = np.isnan(ref.matrix[:, 1:]).any(axis=1) & ~nan0
+    assert nan0.any() and nan_other.any()  # both situations occur
+    m = r.values.reshape(-1, len(v))
+    np.testing.assert_array_equal(_canon(m), _canon(ref.matrix))
+    np.testing.assert_array_equal(r.best_idx.reshape(-1), ref.best_idx)
+    np.testing.assert_array_equal(_canon(r.best_semblance.reshape(-1)), _canon(ref.best_semblance))
+    assert np.all(r.best_idx.reshape(-1)[nan0] == 0)
+    np.testing.assert_array_equal(r.topk_idx.reshape(-1, 3)[:, 0], ref.best_idx)
+    ti = r.topk_idx.reshape(-1, 3)
+    # no NaN other than at flat index 0 is ever ranked
+    ts = r.topk_semblance.reshape(-1, 3)
+    assert not np.isnan(ts[ti != 0]).any()

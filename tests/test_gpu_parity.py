@@ -247,3 +247,29 @@ def test_topk_more_than_candidates(engine, cmp_small):
     r = engine.run_cmp(ds, cfg, topk=5)
     assert np.all(r.topk_idx[..., 3:] == -1)
     assert np.all(np.sort(r.topk_idx[..., :3], axis=-1) == np.arange(3))
+
+
+def test_topk_crs_large_slice_bounded_panel(engine):
+    """Top-k on a 64-midpoint CRS-large slice (18081 candidates): the
+    semblance panel is per wave (<= 4 GB), not the shard's 9.3 GB; top-1 is
+    the pick, the k entries are sorted, and the picks equal a run without
+    top-k bit for bit."""
+    import torch
+    wl = configs.crs_large()
+    wl.config.kernel_variant = "fast"
+    halo = 10
+    ds = wl.spec.generate(first=1000 - halo, count=64 + 2 * halo)
+    plain = engine.run_crs(ds, wl.config, wl.apm, abc=wl.abc, rows=(halo, 64))
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    r = engine.run_crs(ds, wl.config, wl.apm, abc=wl.abc, rows=(halo, 64), topk=4)
+    free1, _ = torch.cuda.mem_get_info()
+    whole = 64 * ds.ns * wl.ncand * 4
+    assert free0 - free1 < 0.6 * whole, (free0 - free1, whole)
+    np.testing.assert_array_equal(r.topk_idx[..., 0], plain.best_idx)
+    np.testing.assert_array_equal(r.best_idx, plain.best_idx)
+    np.testing.assert_array_equal(r.best_semblance.view(np.uint32),
+                                  plain.best_semblance.view(np.uint32))
+    ts = r.topk_semblance
+    assert np.all(ts[..., :-1] >= ts[..., 1:])
+    np.testing.assert_array_equal(ts[..., 0], plain.best_semblance)
