@@ -77,6 +77,7 @@ struct KernelChoice {
   int cc = 0;
   int cap = 0;  // compile-time stage capacity (FAST), 0 = runtime (EXACT)
   size_t slot_bytes = 0;  // plan slots + per-warp moveout terms (dynamic smem)
+  bool quad = false;      // FAST table layout: quads (16 B) instead of pairs (8 B)
 };
 
 // FAST stage capacities (entries): the default, and the one for traces
@@ -90,8 +91,17 @@ constexpr int kFastCap = VELAN_FAST_CAP;
 // aperture exceeds the 227 KB budget and is refused before any launch)
 constexpr int kFastCapBig = (190 * 1024 / (kStages * 16)) / 32 * 32;
 constexpr int kFastMaxNs = kFastCapBig - 48;  // staging_need(ns) <= cap
+// the quad layout's stage (24 B per entry: a float4 quad + the float2
+// energies): two stages in ~166 KB, traces up to 3408 samples.  Experimental
+// (-DVELAN_QUAD): half the window loads, but the LDS.128 destinations cost
+// register moves at 128 registers and it measured 0.5 % slower on CMP large
+// (profiles/round2/experiments.md), so the pair layout is the default.
+#ifndef VELAN_QUAD_CAP
+#define VELAN_QUAD_CAP 3456
+#endif
+constexpr int kQuadCap = VELAN_QUAD_CAP;
 
-template <int OPK, int VAR, int WMAX, bool FIXED, int CAPF = 0>
+template <int OPK, int VAR, int WMAX, bool FIXED, int CAPF = 0, bool QUAD = false>
 KernelChoice pick() {
   // FAST keeps two accumulator rows (P, R) per pair: half the pairs
   // candidates per warp (the group of a CTA is kWarps x CC candidates)
@@ -99,13 +109,32 @@ KernelChoice pick() {
   // measured 1.21x slower on CMP large: instruction count beats occupancy)
   constexpr int CC = WMAX > 16 ? 1 : 2;
   constexpr int CAP = VAR == VAR_FAST ? (CAPF ? CAPF : kFastCap) : 0;
-  return KernelChoice{&semblance_scan_kernel<OPK, VAR, WMAX, FIXED, CC, CAP>, CC, CAP,
+  return KernelChoice{&semblance_scan_kernel<OPK, VAR, WMAX, FIXED, CC, CAP, QUAD>, CC, CAP,
                       2 * kStages * sizeof(PlanSlot) +
-                          sizeof(float) * kWarps * kBatch * qs_row(CC, OpTraits<OPK>::NQ)};
+                          sizeof(float) * kWarps * kBatch * qs_row(CC, OpTraits<OPK>::NQ),
+                      QUAD};
 }
 
 template <int OPK, int VAR>
-KernelChoice pick_w(int w, bool big) {
+KernelChoice pick_w(int w, bool big, bool quad) {
+#ifdef VELAN_QUAD
+  if constexpr (VAR == VAR_FAST) {
+    if (quad) {  // fixed windows, traces that fit the quad stage
+      switch (w) {
+        case 1: return pick<OPK, VAR, 1, true, kQuadCap, true>();
+        case 2: return pick<OPK, VAR, 2, true, kQuadCap, true>();
+        case 4: return pick<OPK, VAR, 4, true, kQuadCap, true>();
+        case 8: return pick<OPK, VAR, 8, true, kQuadCap, true>();
+        case 11: return pick<OPK, VAR, 11, true, kQuadCap, true>();
+        case 15: return pick<OPK, VAR, 15, true, kQuadCap, true>();
+        case 16: return pick<OPK, VAR, 16, true, kQuadCap, true>();
+        default: break;
+      }
+    }
+  }
+#else
+  (void)quad;
+#endif
   if (VAR == VAR_FAST && big) {  // rare: generic windows only
     if (w <= 4) return pick<OPK, VAR, 4, false, kFastCapBig>();
     if (w <= 8) return pick<OPK, VAR, 8, false, kFastCapBig>();
@@ -128,13 +157,24 @@ KernelChoice pick_w(int w, bool big) {
   return pick<OPK, VAR, 32, false>();
 }
 
-KernelChoice choose_kernel(int op, int variant, int w, bool big) {
+bool is_fixed_window(int w) {
+  return w == 1 || w == 2 || w == 4 || w == 8 || w == 11 || w == 15 || w == 16;
+}
+
+int staging_need(int ns, bool fast);
+
+// FAST: the quad layout when the window is a compiled one and a trace fits
+// its stage; the pair layout (larger stage) otherwise.
+KernelChoice choose_kernel(int op, int variant, int w, int ns) {
+  const bool fast = variant == VELAN_VARIANT_FAST;
+  const bool quad = fast && is_fixed_window(w) && staging_need(ns, true) <= kQuadCap;
+  const bool big = fast && staging_need(ns, true) > kFastCap;
   const int opk = op == VELAN_OP_CRS_ABC ? OPK_ABC : OPK_Q;
   if (opk == OPK_Q)
-    return variant == VELAN_VARIANT_EXACT ? pick_w<OPK_Q, VAR_EXACT>(w, big)
-                                          : pick_w<OPK_Q, VAR_FAST>(w, big);
-  return variant == VELAN_VARIANT_EXACT ? pick_w<OPK_ABC, VAR_EXACT>(w, big)
-                                        : pick_w<OPK_ABC, VAR_FAST>(w, big);
+    return variant == VELAN_VARIANT_EXACT ? pick_w<OPK_Q, VAR_EXACT>(w, big, false)
+                                          : pick_w<OPK_Q, VAR_FAST>(w, big, quad);
+  return variant == VELAN_VARIANT_EXACT ? pick_w<OPK_ABC, VAR_EXACT>(w, big, false)
+                                        : pick_w<OPK_ABC, VAR_FAST>(w, big, quad);
 }
 
 // ---------------------------------------------------------------------------
@@ -689,8 +729,7 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
   }
 
   const bool fast = sc->variant == VELAN_VARIANT_FAST;
-  const KernelChoice kc = choose_kernel(h.op, sc->variant, h.w,
-                                        fast && staging_cap(h.ns, true) != kFastCap);
+  const KernelChoice kc = choose_kernel(h.op, sc->variant, h.w, h.ns);
   ScanParams p{};
   p.samples = d_samples;
   p.h2 = D.bufs[B_H2].as<float>();
@@ -717,15 +756,19 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
                : (h.ns % 4 == 0) &&
                      (reinterpret_cast<uintptr_t>(d_samples) % 16 == 0);
   p.cap = kc.cap ? kc.cap : staging_cap(h.ns, fast);
-  float2* d_tab = nullptr;
+  char* d_tab = nullptr;
+  float2* d_ec = nullptr;
   size_t tab_traces = 0;
+  const size_t tab_b = kc.quad ? 16 : 8;  // table entry bytes
   if (fast) {
-    // pairs then energies (8 B per sample each) of one wave's gathers
+    // pairs (quads) then energies of one wave's gathers: 16 (24) B per sample
     tab_traces = static_cast<size_t>(std::max(s.table_span, 1)) * h.M;
-    D.bufs[B_EC].ensure(tab_traces * h.ns * 16 + 64);
-    d_tab = D.bufs[B_EC].as<float2>();
-    p.pairs = d_tab;
-    p.ec = d_tab + tab_traces * h.ns;
+    D.bufs[B_EC].ensure(tab_traces * h.ns * (tab_b + 8) + 64);
+    d_tab = D.bufs[B_EC].as<char>();
+    d_ec = reinterpret_cast<float2*>(d_tab + tab_traces * h.ns * tab_b);
+    p.pairs = reinterpret_cast<const float2*>(d_tab);
+    p.quads = reinterpret_cast<const float4*>(d_tab);
+    p.ec = d_ec;
   }
   p.dt = h.dt;
   {
@@ -750,7 +793,7 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
   const size_t meta_floats = 5 * static_cast<size_t>(max_legs) + max_sweep +
                              h.n_a + h.n_b + h.n_c + 6 * (kWarps - 1) * kT0;
   const size_t smem =
-      (static_cast<size_t>(kStages) * p.cap * (fast ? 4 : 1) + meta_floats) *
+      (static_cast<size_t>(kStages) * p.cap * (fast ? (kc.quad ? 6 : 4) : 1) + meta_floats) *
           sizeof(float) +
       kc.slot_bytes;
   // the kernel's static __shared__ (barriers, planner state) counts against
@@ -793,9 +836,15 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
       tab_hi = s.wave_hi[wv];
       const long long ntr = static_cast<long long>(tab_hi - tab_lo) * h.M;
       dim3 eg(static_cast<unsigned>(ntr), (h.ns + 255) / 256);
-      pair_energy_kernel<<<eg, 256, (256 + h.w + 1) * sizeof(float), st>>>(
-          d_samples + static_cast<size_t>(tab_lo) * trace_floats, d_tab,
-          d_tab + tab_traces * h.ns, ntr, h.ns, h.w);
+      const size_t tsm = (256 + std::max(h.w, 2) + 1) * sizeof(float);
+      if (kc.quad)
+        pair_energy_kernel<true><<<eg, 256, tsm, st>>>(
+            d_samples + static_cast<size_t>(tab_lo) * trace_floats, d_tab, d_ec, ntr, h.ns,
+            h.w);
+      else
+        pair_energy_kernel<false><<<eg, 256, tsm, st>>>(
+            d_samples + static_cast<size_t>(tab_lo) * trace_floats, d_tab, d_ec, ntr, h.ns,
+            h.w);
       VG_CUDA(cudaGetLastError());
       p.table_trace0 = static_cast<long long>(tab_lo) * h.M;
       ++out.launches;
