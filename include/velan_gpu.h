@@ -195,6 +195,20 @@ int velan_gpu_plan_execute(velan_gpu_plan* plan, velan_gpu_result* res,
 int velan_gpu_plan_launches(const velan_gpu_plan* plan);
 void velan_gpu_plan_destroy(velan_gpu_plan* plan);
 
+/* NMO-corrected output gathers: every trace m of output
+ * row r flattened with the row's picks — out[r][m][k] = interpolate(a[k1],
+ * a[k1 + 1], x) (kernel.hpp:39) at hit_for(t, dt, ns, 1) (traveltime.hpp:
+ * 66-80: k1 = floor(t / dt), x its fraction, 0 outside the trace) of the
+ * central gather's traveltime t = crs_traveltime(t0_k, h2_m, 0, v)
+ * (traveltime.hpp:53-56) for the pick's velocity v = v[picks[r][k] % n_c]
+ * (for CRS_ABC at dm = 0 the operator is that same NMO expression bit for
+ * bit).  Rows are the scan's output rows (row order and row_first /
+ * row_count as for the scan); picks [rows][ns] host, out [rows][max_traces]
+ * [ns] host, traces past a gather's count zero.  The stacked, corrected
+ * trace is the mean over m.  Single device (the context's first). */
+int velan_gpu_nmo_correct(velan_gpu_ctx* ctx, const velan_gpu_dataset* ds,
+                          const velan_gpu_scan* sc, const int32_t* picks, float* out);
+
 /* hit_for (traveltime.hpp:66-80) evaluated by the device code path of the
  * given variant, for n traveltimes t (host arrays).  Test hook for the
  * index arithmetic: k1 and valid must match the reference bit for bit. */

@@ -57,6 +57,9 @@ def oracle_lib() -> C.CDLL:
         lib.vo_interpolate.argtypes = [C.c_float, C.c_float, C.c_float]
         lib.vo_halfpoint.restype = C.c_float
         lib.vo_halfpoint.argtypes = [C.c_float] * 4
+        lib.vo_nmo_correct.restype = None
+        lib.vo_nmo_correct.argtypes = [_P, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_uint32,
+                                       C.c_int, _P, C.c_int, _P, _P]
         lib.vo_row_order.restype = None
         lib.vo_row_order.argtypes = [_P, C.c_int, C.c_int, _P]
         _oracle = lib
@@ -195,6 +198,19 @@ def run_cells(ds, op: str, w: int, v, rows, ks, apm: float = 0.0, abc=None,
         raise ValueError("oracle: invalid configuration")
     out = CellResult(bi, bs, bst, mat, int(valid.value))
     out.stack_matrix = smat
+    return out
+
+
+def nmo_correct(ds, op: str, v, picks) -> np.ndarray:
+    """vo_nmo_correct: the corrected gathers [G, M, ns] of all rows."""
+    lib = oracle_lib()
+    samples, coords, ntr, ids = _flat(ds)
+    G, M, ns = samples.shape
+    vv = np.ascontiguousarray(v, np.float32)
+    picks = np.ascontiguousarray(picks, np.int32)
+    out = np.zeros((G, M, ns), np.float32)
+    lib.vo_nmo_correct(_p(samples), _p(coords), _p(ntr), _p(ids), G, M, ns, int(ds.dt_us),
+                       OP[op], _p(vv), len(vv), _p(picks), _p(out))
     return out
 
 

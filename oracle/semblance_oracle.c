@@ -816,6 +816,40 @@ int vo_run_cells(const float* samples, const float* coords,
   return 0;
 }
 
+/* NMO-corrected gathers (the GPU's velan_gpu_nmo_correct):
+ * out[r][m][k] = interpolate(a[k1], a[k1+1], x) at hit_for(t, dt, ns, 1) of
+ * t = crs_traveltime(t0_k, h2_m, 0, v[pick % n_c]) (traveltime.hpp:53-80,
+ * kernel.hpp:39); 0 outside the trace and for traces past ntraces.  Rows in
+ * output order (vo_row_order for op). */
+void vo_nmo_correct(const float* samples, const float* coords, const int32_t* ntraces,
+                    const uint32_t* cdp_id, int G, int M, int ns, uint32_t dt_us, int op,
+                    const float* v, int n_c, const int32_t* picks, float* out) {
+  const double dt = (double)dt_us * 1e-6;
+  int32_t* rows = (int32_t*)malloc(sizeof(int32_t) * (size_t)(G + 1));
+  vo_row_order(cdp_id, G, op, rows);
+  for (int r = 0; r < G; ++r) {
+    const int g = rows[r];
+    for (int m = 0; m < M; ++m) {
+      float* o = out + ((size_t)r * M + m) * (size_t)ns;
+      if (m >= ntraces[g]) {
+        for (int k = 0; k < ns; ++k) o[k] = 0.0f;
+        continue;
+      }
+      const float* c4 = coords + ((size_t)g * M + m) * 4;
+      const float h2 = vo_halfpoint(c4[0], c4[1], c4[2], c4[3]);
+      const float* a = samples + ((size_t)g * M + m) * (size_t)ns;
+      for (int k = 0; k < ns; ++k) {
+        const int c = picks[(size_t)r * ns + k];
+        const float t0 = (float)(k * dt);
+        const float t = vo_traveltime_q(t0, h2, 0.0f, v[((c % n_c) + n_c) % n_c]);
+        const vo_hit hit = vo_hit_for(t, dt, ns, 1);
+        o[k] = hit.valid ? vo_interpolate(a[hit.k1], a[hit.k1 + 1], hit.x) : 0.0f;
+      }
+    }
+  }
+  free(rows);
+}
+
 /* Batch helpers for the golden / known-answer tests. */
 void vo_hit_batch(const float* t, int n, double dt_s, int ns, int w,
                   int32_t* k1, float* x, uint8_t* valid) {

@@ -131,6 +131,7 @@ SIGNATURES = {
     "velan_gpu_plan_execute": (C.c_int, [_P, C.POINTER(Result), _P]),
     "velan_gpu_plan_launches": (C.c_int, [_P]),
     "velan_gpu_plan_destroy": (None, [_P]),
+    "velan_gpu_nmo_correct": (C.c_int, [_P, C.POINTER(Dataset), C.POINTER(Scan), _P, _P]),
     "velan_gpu_hit_batch": (C.c_int, [_P, C.c_int32, C.c_double, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P]),
     "velan_gpu_synth_generate": (C.c_int, [C.POINTER(Synth), _P, _P, _P, _P]),
     "velan_gpu_synth_generate_device": (C.c_int, [C.POINTER(Synth), _P, _P]),

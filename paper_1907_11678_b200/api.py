@@ -406,6 +406,30 @@ class Engine:
                          config.w, config.grid(), abc, apm, emit_matrix, out,
                          rows, topk)
 
+    def nmo_correct(self, ds: Dataset, config: ScanConfig, picks,
+                    op: str = "nmo", apm: float = 0.0,
+                    abc: Optional[CrsAbcGrid] = None, rows=None) -> np.ndarray:
+        """NMO-corrected output gathers [rows, max_traces, ns] of a scan's
+        picks (``picks`` = ScanResult.best_idx or any [rows, ns] flat
+        candidate indices): each trace interpolated (kernel.hpp:39) at the
+        central traveltime of its row's pick (traveltime.hpp:53-80); the
+        mean over the traces is the corrected stack."""
+        lib = N.load()
+        config.validate()
+        opc = {"nmo": N.OP_NMO, "d2": N.OP_CRS_D2, "abc": N.OP_CRS_ABC}[op]
+        keep: list = []
+        sc = _scan_struct(opc, config.kernel_variant, config.w, config.grid(), abc, apm,
+                          keep, rows)
+        dss = _dataset_struct(ds)
+        n_rows = ds.ncdps if rows is None else int(rows[1])
+        picks = np.ascontiguousarray(picks, np.int32)
+        if picks.shape != (n_rows, dss.ns):
+            raise ParameterError(f"picks must be [{n_rows}, {dss.ns}]")
+        out = np.zeros((n_rows, max(ds.fold, 1), dss.ns), np.float32)
+        _raise(lib.velan_gpu_nmo_correct(self._h, C.byref(dss), C.byref(sc), _ptr(picks),
+                                         _ptr(out)), "velan_gpu_nmo_correct")
+        return out
+
     def plan(self, ds: Dataset, config: ScanConfig, op: str = "nmo",
              apm: float = 0.0, abc: Optional[CrsAbcGrid] = None,
              rows: Optional[tuple] = None) -> "Plan":

@@ -1319,6 +1319,90 @@ __global__ void hit_batch_kernel(const float* t, int n, double dt, int ns,
 }  // namespace
 }  // namespace velan_gpu
 
+namespace velan_gpu {
+namespace {
+// One block per (row, trace), threads over the output samples: the trace is
+// read once into shared memory, every output sample interpolates it at the
+// pick's traveltime with the reference's rounding (crs_traveltime, hit_for,
+// interpolate — no contraction).
+__global__ void __launch_bounds__(256)
+    nmo_correct_kernel(const float* __restrict__ samples, const float* __restrict__ h2,
+                       const int* __restrict__ ntr, const int* __restrict__ row_gather,
+                       const int32_t* __restrict__ picks, const float* __restrict__ t0,
+                       const float* __restrict__ v, int n_c, int Mmax, int ns, double dt,
+                       float* __restrict__ out) {
+  extern __shared__ float tr[];
+  const int r = blockIdx.y, m = blockIdx.x;
+  const int g = row_gather[r];
+  float* o = out + (static_cast<size_t>(r) * Mmax + m) * ns;
+  if (m >= ntr[g]) {
+    for (int k = threadIdx.x; k < ns; k += blockDim.x) o[k] = 0.0f;
+    return;
+  }
+  const float* a = samples + (static_cast<size_t>(g) * Mmax + m) * ns;
+  for (int k = threadIdx.x; k < ns; k += blockDim.x) tr[k] = a[k];
+  __syncthreads();
+  const float hh = h2[static_cast<size_t>(g) * Mmax + m];
+  for (int k = threadIdx.x; k < ns; k += blockDim.x) {
+    const int c = picks[static_cast<size_t>(r) * ns + k];
+    const float vv = v[((c % n_c) + n_c) % n_c];
+    const float t = tt_q(__fmul_rn(t0[k], t0[k]), moveout_q(hh, 0.0f, vv));
+    int k1;
+    float x;
+    bool valid;
+    hit_exact(t, dt, ns, 1, k1, x, valid);
+    o[k] = valid ? __fadd_rn(__fmul_rn(__fsub_rn(tr[k1 + 1], tr[k1]), x), tr[k1]) : 0.0f;
+  }
+}
+}  // namespace
+}  // namespace velan_gpu
+
+extern "C" int velan_gpu_nmo_correct(velan_gpu_ctx* ctx, const velan_gpu_dataset* ds,
+                                     const velan_gpu_scan* sc, const int32_t* picks,
+                                     float* out) {
+  VG_API_BEGIN
+  if (!ctx) throw ApiError(VELAN_GPU_EPARAM, "null context");
+  validate(ds, sc, sc && sc->op != VELAN_OP_NMO);
+  if (ds->n_gathers == 0) return VELAN_GPU_OK;
+  if (!picks || !out) throw ApiError(VELAN_GPU_EPARAM, "picks or out is null");
+  if (ds->samples_mem != VELAN_MEM_HOST)
+    throw ApiError(VELAN_GPU_EPARAM, "velan_gpu_nmo_correct: samples must be host memory");
+  const HostSweep h = build_sweep(ds, sc);
+  if (h.rows == 0) return VELAN_GPU_OK;
+  for (size_t i = 0; i < static_cast<size_t>(h.rows) * h.ns; ++i)
+    if (picks[i] < 0 || picks[i] >= h.ncand)
+      throw ApiError(VELAN_GPU_EPARAM, "pick index outside the candidate grid");
+  std::lock_guard<std::mutex> guard(ctx->lock);
+  DeviceState& D = ctx->devs[0];
+  VG_CUDA(cudaSetDevice(D.dev));
+  cudaStream_t st = D.stream;
+  const size_t tf = static_cast<size_t>(h.M) * h.ns;
+  std::vector<int> ntr(ds->ntraces, ds->ntraces + h.G);
+  D.bufs[B_SAMPLES].ensure(static_cast<size_t>(h.G) * tf * 4 + 64);
+  VG_CUDA(cudaMemcpyAsync(D.bufs[B_SAMPLES].p, ds->samples, static_cast<size_t>(h.G) * tf * 4,
+                          cudaMemcpyHostToDevice, st));
+  upload(D.bufs[B_H2], h.h2, st);
+  upload(D.bufs[B_NTR], ntr, st);
+  upload(D.bufs[B_LEGG], h.row_gather, st);
+  upload(D.bufs[B_T0], h.t0, st);
+  upload(D.bufs[B_V], h.v, st);
+  const size_t cells = static_cast<size_t>(h.rows) * h.ns;
+  D.bufs[B_BIDX].ensure(cells * 4);
+  VG_CUDA(cudaMemcpyAsync(D.bufs[B_BIDX].p, picks, cells * 4, cudaMemcpyHostToDevice, st));
+  D.bufs[B_MAT].ensure(static_cast<size_t>(h.rows) * tf * 4);
+  dim3 grid(static_cast<unsigned>(h.M), static_cast<unsigned>(h.rows));
+  nmo_correct_kernel<<<grid, 256, h.ns * sizeof(float), st>>>(
+      D.bufs[B_SAMPLES].as<float>(), D.bufs[B_H2].as<float>(), D.bufs[B_NTR].as<int>(),
+      D.bufs[B_LEGG].as<int>(), D.bufs[B_BIDX].as<int32_t>(), D.bufs[B_T0].as<float>(),
+      D.bufs[B_V].as<float>(), h.n_c, h.M, h.ns, h.dt, D.bufs[B_MAT].as<float>());
+  VG_CUDA(cudaGetLastError());
+  VG_CUDA(cudaMemcpyAsync(out, D.bufs[B_MAT].p, static_cast<size_t>(h.rows) * tf * 4,
+                          cudaMemcpyDeviceToHost, st));
+  VG_CUDA(cudaStreamSynchronize(st));
+  return VELAN_GPU_OK;
+  VG_API_END
+}
+
 extern "C" int velan_gpu_hit_batch(const float* t, int32_t n, double dt_s,
                                    int32_t ns, int32_t w, int32_t variant,
                                    int32_t* k1, float* x, uint8_t* valid) {

@@ -273,3 +273,45 @@ def test_topk_crs_large_slice_bounded_panel(engine):
     ts = r.topk_semblance
     assert np.all(ts[..., :-1] >= ts[..., 1:])
     np.testing.assert_array_equal(ts[..., 0], plain.best_semblance)
+
+
+@pytest.mark.parametrize("op", ["nmo", "abc"])
+def test_nmo_corrected_gathers_match_oracle(engine, op):
+    """NMO-corrected output gathers from the scan's own
+    picks: bitwise equal to the oracle's restatement (crs_traveltime at the
+    pick, hit_for with w = 1, interpolate), ragged traces zero."""
+    if op == "nmo":
+        wl = configs.cmp_small()
+        ds = wl.spec.generate(count=6)
+        ds.ntraces[2] = 17
+        cfg = ScanConfig(w=11, velocities=wl.config.grid(), kernel_variant="fast")
+        r = engine.run_cmp(ds, cfg)
+        out = engine.nmo_correct(ds, cfg, r.best_idx)
+        ref = oracle.nmo_correct(ds, "nmo", cfg.grid(), r.best_idx)
+        assert np.all(out[2, 17:] == 0)
+    else:
+        wl = configs.crs_small()
+        ds = wl.spec.generate(first=50, count=12)
+        grid = CrsAbcGrid(wl.abc.a[::5], wl.abc.b[::5], wl.abc.v)
+        cfg = ScanConfig(w=11, velocities=grid.v, kernel_variant="fast")
+        r = engine.run_crs(ds, cfg, wl.apm, abc=grid)
+        out = engine.nmo_correct(ds, cfg, r.best_idx, op="abc", apm=wl.apm, abc=grid)
+        ref = oracle.nmo_correct(ds, "abc", grid.v, r.best_idx)
+    np.testing.assert_array_equal(out.view(np.uint32), ref.view(np.uint32))
+
+
+def test_nmo_correction_flattens_a_planted_event(engine):
+    """A noiseless hyperbolic event at v = 2500 m/s: corrected with the picks
+    the scan finds, every trace peaks at the event's zero-offset time."""
+    from helpers import reference_synthetic
+    ds = reference_synthetic(2, 24, 1500, 1000, [(0.6, 2500.0, 1.0), (1.1, 3000.0, 0.8)],
+                             wavelet_freq=25.0, max_offset=1200.0)
+    cfg = ScanConfig(w=11, velocities=velocity_grid(2000.0, 3500.0, 31), kernel_variant="fast")
+    r = engine.run_cmp(ds, cfg)
+    out = engine.nmo_correct(ds, cfg, r.best_idx)
+    for t0 in (0.6, 1.1):
+        k = int(round(t0 / 1e-3))
+        win = out[:, 1:, k - 20:k + 21]  # trace 0 is zero offset already
+        assert np.all(np.abs(np.argmax(win, axis=2) - 20) <= 1)
+        # and the uncorrected far traces do not peak there
+        assert np.argmax(ds.samples[0, -1, k - 20:k + 21]) != 20
