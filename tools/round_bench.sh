@@ -1,23 +1,28 @@
 #!/bin/bash
-# One GPU call: the default bench, other workloads, the reference arm, the
-# torchrun path, the ncu launch list + DRAM traffic of the default bench
-# command and one full-set capture of the scan kernel.
+# One GPU call: the evidence of a round — the default bench (CMP large +
+# the crs_small sub-record), the other workloads, both reference arms, the
+# EXACT variant, the --gpus / torchrun paths at N = 1, the ncu launch list
+# with DRAM bytes of the bench command, and full-set captures of the scan
+# kernel.  usage: tools/round_bench.sh OUT
+O=${1:-gpurun_out/round}; mkdir -p $O
 set -x
-mkdir -p gpurun_out/rb3
-python bench.py > gpurun_out/rb3/bench_default.json 2> gpurun_out/rb3/bench_default.err
-python bench.py --workload cmp_small --cpu-seconds 5 > gpurun_out/rb3/bench_cmp_small.json 2> gpurun_out/rb3/bench_cmp_small.err
-python bench.py --workload crs_small --steps 2 --warmup 3 --cpu-seconds 10 > gpurun_out/rb3/bench_crs_small.json 2> gpurun_out/rb3/bench_crs_small.err
-python bench.py --workload crs_large --gathers 64 --steps 1 --warmup 3 --no-e2e --cpu-seconds 10 > gpurun_out/rb3/bench_crs_large64.json 2> gpurun_out/rb3/bench_crs_large64.err
-python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/rb3/bench_reference.json 2> gpurun_out/rb3/bench_reference.err
-python bench.py --variant exact --steps 1 --warmup 3 --no-e2e --no-cpu > gpurun_out/rb3/bench_exact.json 2> gpurun_out/rb3/bench_exact.err
+python bench.py --steps 10 --warmup 3 > $O/bench_default.json 2> $O/bench_default.err
+python bench.py --workload cmp_small --cpu-seconds 5 > $O/bench_cmp_small.json 2> $O/bench_cmp_small.err
+python bench.py --workload crs_large --gathers 256 --steps 1 --warmup 1 > $O/bench_crs_large256.json 2> $O/bench_crs_large256.err
+python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err
+python bench.py --impl reference --workload crs_small --steps 3 --warmup 1 > $O/bench_reference_crs_small.json 2> $O/bench_reference_crs_small.err
+python bench.py --variant exact --steps 1 --warmup 3 --no-e2e --no-cpu --no-sub > $O/bench_exact.json 2> $O/bench_exact.err
+python bench.py --gpus 1 --steps 2 --warmup 3 --no-cpu --no-sub > $O/bench_gpus1.json 2> $O/bench_gpus1.err
 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29517 \
-    bench.py --gpus 1 --steps 2 --warmup 3 --no-cpu > gpurun_out/rb3/bench_torchrun1.json 2> gpurun_out/rb3/bench_torchrun1.err
-# ncu: launch list (every launch, device time) and DRAM bytes of the default command
-python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/rb3/plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-    --log-file gpurun_out/rb3/launches.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/rb3/ncu_launch.log 2>&1
-# one full-set capture of the scan kernel on a CMP-large slice
-python bench.py --workload cmp_large --gathers 256 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/rb3/slice.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:semblance_scan -c 1 -o gpurun_out/rb3/prof_final3 \
-    python bench.py --workload cmp_large --gathers 256 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/rb3/ncu_full.log 2>&1
+    bench.py --gpus 1 --steps 2 --warmup 3 --no-cpu --no-sub > $O/bench_torchrun1.json 2> $O/bench_torchrun1.err
+for WL in "cmp_large 8192" "crs_small 256"; do
+  set -- $WL
+  CMD="python bench.py --workload $1 --steps 1 --warmup 1 --no-e2e --no-cpu --no-parity --no-sub"
+  $CMD > $O/plain_$1.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+      --log-file $O/launches_$1.csv $CMD > $O/ncu_launch_$1.log 2>&1
+done
+./tools/ncu_cmp.sh $O cmp_large 148
+./tools/ncu_cmp.sh $O crs_small 32
+./tools/ncu_cmp.sh $O crs_large 12
 echo done
