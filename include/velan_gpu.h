@@ -191,7 +191,8 @@ int velan_gpu_plan_create(velan_gpu_ctx* ctx, const velan_gpu_dataset* ds,
                           const velan_gpu_scan* sc, velan_gpu_plan** out);
 int velan_gpu_plan_execute(velan_gpu_plan* plan, velan_gpu_result* res,
                            void* stream);
-/* Kernel launches one execute issues (for launch accounting). */
+/* Kernel launches the last execute issued (scan waves, FAST table passes,
+ * top-k; for launch accounting); before the first execute, the scan waves. */
 int velan_gpu_plan_launches(const velan_gpu_plan* plan);
 void velan_gpu_plan_destroy(velan_gpu_plan* plan);
 

@@ -1271,6 +1271,9 @@ int velan_gpu_plan_execute(velan_gpu_plan* plan, velan_gpu_result* res,
 
 int velan_gpu_plan_launches(const velan_gpu_plan* plan) {
   if (!plan) return 0;
+  // the last execute's kernel launches (scan waves + FAST table passes +
+  // top-k); before any execute, the scan waves alone
+  if (plan->launches > 0) return plan->launches;
   return static_cast<int>(plan->shard.wave_need.size());
 }
 
