@@ -191,16 +191,19 @@ def algorithmic_flops(valid: int, nominal: int, w: int) -> float:
 
 
 def load_traffic(workload: str):
+    """DRAM bytes (read + write) of the scan kernel per launch and per step,
+    from the committed ncu launch list of the same command
+    (profiles/traffic.json, tools/traffic_from_launches.py)."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        e = d.get(workload)
-        # DRAM bytes (read + write) of the scan kernel per step, from the
-        # committed ncu launch list of the same command
-        return None if e is None else float(e["dram_bytes_per_step"])
+            e = json.load(f).get(workload)
+        if e is None:
+            return None, None
+        step = float(e["dram_bytes_per_step"])
+        return step / max(int(e.get("scan_launches_per_step", 1)), 1), step
     except Exception:
-        return None
+        return None, None
 
 
 def _proxy_velocities(wl):
@@ -596,7 +599,7 @@ def measure(ctx: Ctx, args, wl_name: str, steps: int, warmup: int, sub: bool = F
     import ctypes as C
     pm = C.c_double(0.0)
     _native.load().velan_gpu_measure_fp32_peak(local, C.byref(pm))
-    traffic = load_traffic(wl.name)
+    traffic, traffic_step = load_traffic(wl.name)
 
     # ---- gather the picks of every rank to rank 0's host memory ----------
     t_gather = time.perf_counter()
@@ -691,6 +694,10 @@ def measure(ctx: Ctx, args, wl_name: str, steps: int, warmup: int, sub: bool = F
             "roofline": {"bound": "fp32", "achieved": achieved_tf, "peak": nominal_peak,
                          "unit": "TFLOP/s", "frac": achieved_tf / nominal_peak,
                          "traffic": traffic,
+                         "traffic_per_step": traffic_step,
+                         "traffic_source": "profiles/traffic.json (ncu launch list, "
+                                           "dram__bytes_read + dram__bytes_write of the "
+                                           "scan kernel, per launch)",
                          "peak_source": "nominal FP32 FMA peak 2 x 128 x SMs x 1965 MHz "
                                         "(MEASURED_PEAKS.json has no FP32 figure)",
                          "measured_fma_peak": pm.value,
