@@ -325,12 +325,8 @@ def parity_sample(wl, n_line: int, line_rows, picks, n_cells: int = 0, seed: int
             ks = np.sort(rng.choice(ns, per, replace=False)).astype(np.int32)
             groups.append((int(r), ks))
         # the sampled gathers, generated like the ranks generated them
-        samples = []
-        for r, ks in groups:
-            g = int(line_rows[r])
-            samples.append((r, g, ks))
+        samples = [(r, int(line_rows[r]), ks) for r, ks in groups]
         gl = [g for _, g, _ in samples]
-        ds = None
         parts = [wl.spec.generate(first=g, count=1, n_line=n_line, lib=lib) for g in gl]
         ds = _concat(parts)
         crow = np.concatenate([np.full(len(ks), i, np.int32) for i, (_, _, ks) in enumerate(samples)])
@@ -356,7 +352,6 @@ def parity_sample(wl, n_line: int, line_rows, picks, n_cells: int = 0, seed: int
                                      ck[sl], mode=2, matrix=True)
             _reduce_chunk(r, gidx_all[sl], sl, ref_idx, ref_s, ref_st, ref_at, gap)
         samples_abs = float(np.abs(ds.samples).max())
-        src = (ds, crow, ck)
         n_rows_s = len(groups)
     else:
         n_target = n_cells or 4096
@@ -367,7 +362,6 @@ def parity_sample(wl, n_line: int, line_rows, picks, n_cells: int = 0, seed: int
         kind = "port (oracle mode 2, the fp32 operator order; bitwise mode 0)"
         ref_idx, ref_s, ref_st, ref_at, gap, gr_l, ck_l = [], [], [], [], [], [], []
         samples_abs = 0.0
-        mism_src = []
         for r in rows:
             g = int(line_rows[r])
             lo, hi = max(0, g - halo), min(n_line, g + halo + 1)
@@ -387,11 +381,9 @@ def parity_sample(wl, n_line: int, line_rows, picks, n_cells: int = 0, seed: int
             ref_idx.append(o_idx), ref_s.append(o_s), ref_st.append(o_st)
             ref_at.append(o_at), gap.append(o_gap)
             gr_l.append(np.full(n, r, np.int64)), ck_l.append(ks)
-            mism_src.append((ds, crow, ks))
         ref_idx, ref_s, ref_st = np.concatenate(ref_idx), np.concatenate(ref_s), np.concatenate(ref_st)
         ref_at, gap = np.concatenate(ref_at), np.concatenate(gap)
         gr, ck = np.concatenate(gr_l), np.concatenate(ck_l)
-        src = None
         n_rows_s = n_r
     g_idx = bi[gr, ck]
     g_s = bs[gr, ck].astype(np.float64)
