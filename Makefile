@@ -20,7 +20,7 @@ $(LIB): $(SRC) $(HDR)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) -lpthread 2> paper_1907_11678_b200/_lib/ptxas.log || (cat paper_1907_11678_b200/_lib/ptxas.log; exit 1)
 
-oracle:
+oracle: lib
 	$(MAKE) -C oracle
 
 clean:
