@@ -78,6 +78,7 @@ struct KernelChoice {
   int cap = 0;  // compile-time stage capacity (FAST), 0 = runtime (EXACT)
   size_t slot_bytes = 0;  // plan slots + per-warp moveout terms (dynamic smem)
   bool quad = false;      // FAST table layout: quads (16 B) instead of pairs (8 B)
+  int wmax = 0;           // compiled window bound (sizes the split-group scratch)
 };
 
 // FAST stage capacities (entries): the default, and the one for traces
@@ -112,7 +113,7 @@ KernelChoice pick() {
   return KernelChoice{&semblance_scan_kernel<OPK, VAR, WMAX, FIXED, CC, CAP, QUAD>, CC, CAP,
                       2 * kStages * sizeof(PlanSlot) +
                           sizeof(float) * kWarps * kBatch * qs_row(CC, OpTraits<OPK>::NQ),
-                      QUAD};
+                      QUAD, WMAX};
 }
 
 template <int OPK, int VAR>
@@ -792,10 +793,28 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
   // + the consumers' per-tile argmax scratch [2][3][kWarps - 1][kT0]
   const size_t meta_floats = 5 * static_cast<size_t>(max_legs) + max_sweep +
                              h.n_a + h.n_b + h.n_c + 6 * (kWarps - 1) * kT0;
-  const size_t smem =
+  size_t smem =
       (static_cast<size_t>(kStages) * p.cap * (fast ? (kc.quad ? 6 : 4) : 1) + meta_floats) *
           sizeof(float) +
       kc.slot_bytes;
+  // A last candidate group that fills at most half of the consumer warps is
+  // swept by two warps per candidate pair (half a batch each; FAST, two
+  // candidates per warp): the helpers' partial sums go through a scratch of
+  // [consumer warps / 2][2][w + 2][32] floats — when the budget has room
+  p.tail_split = 0;
+  if (fast && kc.cc == 2 && h.op != VELAN_OP_CRS_ABC) {
+    const int cg = (kWarps - 1) * kc.cc;
+    const int rem = h.ncand % cg ? h.ncand % cg : cg;
+    const size_t merge_bytes =
+        sizeof(float) * ((kWarps - 1) / 2) * kc.cc * (kc.wmax + 2) * kT0;
+    cudaFuncAttributes fa0{};
+    VG_CUDA(cudaFuncGetAttributes(&fa0, reinterpret_cast<const void*>(kc.fn)));
+    if (2 * ((rem + kc.cc - 1) / kc.cc) <= kWarps - 1 &&
+        smem + merge_bytes + fa0.sharedSizeBytes <= 227 * 1024) {
+      p.tail_split = 1;
+      smem += merge_bytes;
+    }
+  }
   // the kernel's static __shared__ (barriers, planner state) counts against
   // the same 227 KB opt-in limit as the dynamic allocation
   cudaFuncAttributes fa{};
