@@ -777,6 +777,17 @@ RunOut run_shard(DeviceState& D, const HostSweep& h, const Shard& s,
     p.inv_hi = static_cast<float>(inv);
     p.inv_lo = static_cast<float>(inv - static_cast<double>(p.inv_hi));
     p.amb_eps = static_cast<float>(std::ldexp(std::max(h.ns, 16), -40));
+    // Exact quotient: 1/dt is an integer N (a float) and dt = (1 + e)/N with
+    // |e| < 2^-54.  Then for every float t the double t N is exact (<= 24 +
+    // 20 bits) and |t N e| is below half an ulp of it, so hit_for's
+    // double(t) / dt (traveltime.hpp:66-80) rounds to t N itself: the FAST
+    // hit (floor and fraction of the exact product) equals the reference's
+    // bit for bit and needs no near-integer fix-up.  dt = 1, 2, 4 ms ...
+    const double n = std::nearbyint(inv);
+    p.exact_q = (inv == n && n >= 1.0 && n <= 1048576.0 &&
+                 std::fabs(std::fma(h.dt, n, -1.0)) < std::ldexp(1.0, -54))
+                    ? 1
+                    : 0;
   }
   p.best_idx = d_bidx;
   p.best_s = d_bs;

@@ -101,3 +101,32 @@ def test_block_and_halo_shards():
     assert sh[3].gathers == (65, 100)
     ws = weak_shard(8192, 2, halo=10, world=4)
     assert ws.block == (16384, 24576) and ws.gathers == (16374, 24586)
+
+
+def test_exact_quotient_predicate():
+    """The FAST kernels skip hit_for's near-integer fix-up when the host
+    proves double(t) / dt == t * N for every float t (velan_gpu.cu, `exact_q`:
+    1/dt an integer N <= 2^20 and |dt N - 1| < 2^-54).  Restated here with
+    exact rationals and checked by brute force: where the predicate holds the
+    double quotient of traveltime.hpp:66-80 equals the exact product on two
+    million float traveltimes (so floor and fraction of the product are the
+    reference's), and the inexact sample intervals of the random GPU tests
+    fail it (they keep the fix-up path)."""
+    from fractions import Fraction
+
+    def exact_q(dt_us):
+        dt = float(dt_us) * 1e-6          # CdpGather::dt_seconds
+        inv = 1.0 / dt
+        n = float(np.rint(inv))
+        return (inv == n and 1.0 <= n <= 1048576.0 and
+                abs(Fraction(dt) * Fraction(n) - 1) < Fraction(1, 2 ** 54)), dt, n
+
+    rng = np.random.default_rng(5)
+    t = np.concatenate([rng.uniform(0.0, 16.0, 2_000_000),
+                        rng.uniform(0.0, 1e-3, 100_000)]).astype(np.float32).astype(np.float64)
+    for us in (125, 250, 500, 1000, 2000, 4000, 8000):
+        ok, dt, n = exact_q(us)
+        assert ok, us
+        assert np.array_equal(t / dt, t * n), us
+    for us in (244, 1500, 3333):
+        assert not exact_q(us)[0], us
