@@ -97,6 +97,9 @@ constexpr int kFastMaxNs = kFastCapBig - 48;  // staging_need(ns) <= cap
 // (-DVELAN_QUAD): half the window loads, but the LDS.128 destinations cost
 // register moves at 128 registers and it measured 0.5 % slower on CMP large
 // (profiles/round2/experiments.md), so the pair layout is the default.
+#ifdef VELAN_QUAD
+#error "the experimental quad layout is stale: it fails parity since the byte-offset / exact-quotient hits (profiles/round2/experiments.md); do not build with -DVELAN_QUAD"
+#endif
 #ifndef VELAN_QUAD_CAP
 #define VELAN_QUAD_CAP 3456
 #endif
